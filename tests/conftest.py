@@ -1,0 +1,30 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (runs under gpurun / the driver's GPU tier)")
+    config.addinivalue_line("markers", "slow: long CPU sweeps (HGM_SLOW=1 to run)")
+
+
+def pytest_collection_modifyitems(config, items):
+    if os.environ.get("HGM_SLOW") == "1":
+        return
+    skip = pytest.mark.skip(reason="slow sweep; set HGM_SLOW=1")
+    for it in items:
+        if "slow" in it.keywords:
+            it.add_marker(skip)
+
+
+PARAMS = dict(lambda1=0.6, lambda2=0.2, lambda3=5.0, w_dummy=1.0, T=10)
+
+
+@pytest.fixture
+def params():
+    return dict(PARAMS)

@@ -1,0 +1,221 @@
+"""Pins of the oracle's exact DP (Eqs. 10-13) against brute force,
+closed-form special cases and invariants."""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from oracle import NodeSet, exhaustive
+from tests._tiny import as_dict, tiny_instance
+
+N_MICRO = int(os.environ.get("HGM_MICRO", "300"))
+
+
+# ----------------------------------------------------------- exhaustive sweep
+@pytest.mark.parametrize("chunk", range(4))
+def test_dp_equals_exhaustive_enumeration(chunk):
+    """Micro sweep (S:L521 acceptance 1 shape): M in [1,5], S in [1,7], F in [1,3],
+    T in [1,5], W^d in {0.1,0.5,1,3}, integer pixels; DP optimum = (S+1)^M
+    enumeration with the declarative predicate, and the assignment is the
+    lexicographically smallest optimum whenever the optimum is unique by margin."""
+    for seed in range(chunk, N_MICRO, 4):
+        model, scene, p = tiny_instance(seed)
+        E, Er, A, z = oracle.match(model, scene, p)
+        Eb, zb, nfeas, second = exhaustive.exhaustive_match(as_dict(model), as_dict(scene), p)
+        assert E == pytest.approx(Eb, rel=1e-9, abs=1e-12), seed
+        zz = [None if v < 0 else int(v) for v in z]
+        assert exhaustive.feasible(as_dict(scene), p["T"], zz), seed
+        assert exhaustive.energy(as_dict(model), as_dict(scene), p, zz) == pytest.approx(Eb, rel=1e-9, abs=1e-12)
+        assert Er == pytest.approx(E, rel=1e-12, abs=1e-12)  # E(z_hat) = E*
+        if second - Eb > 1e-9:
+            assert list(z) == list(zb), seed
+
+
+def test_dfs_brute_equals_exhaustive():
+    """The DFS enumerator (C) against the pure-Python enumeration, incl. leaf counts."""
+    for seed in range(120):
+        model, scene, p = tiny_instance(1000 + seed, M_range=(1, 4), S_range=(1, 6))
+        Eb, zb, nfeas, second = exhaustive.exhaustive_match(as_dict(model), as_dict(scene), p)
+        Ed, zd, leaves = oracle.brute(model, scene, p, prune=False)
+        assert leaves == nfeas, seed  # DFS enumerates exactly the feasible set
+        assert Ed == pytest.approx(Eb, rel=1e-9, abs=1e-12)
+        if second - Eb > 1e-9:
+            assert list(zd) == list(zb)
+
+
+def _c0(seed, T=5):
+    wl = synth.make_workload("C0", seed=seed, T=T)
+    model = oracle.model_nodes(wl.models[0])
+    order, scene = oracle.scene_nodes(wl.scenes[0])
+    wb, we = oracle.window_range(scene.t, 0, wl.window)
+    return model, scene.slice(wb, we), wl.params(), wl, order
+
+
+@pytest.mark.parametrize("seed", range(100))
+def test_dp_equals_dfs_brute_C0(seed):
+    """C0 (M=8, ~40 scene points, T=5): DP optimum = exact DFS optimum."""
+    model, scene, p, _, _ = _c0(seed)
+    E, Er, A, z = oracle.match(model, scene, p)
+    Eb, zb, _ = oracle.brute(model, scene, p, prune=True)
+    assert E == pytest.approx(Eb, rel=1e-9)
+    assert oracle.feasible(model, scene, p, z)
+    assert oracle.energy(model, scene, p, z) == pytest.approx(Eb, rel=1e-9)
+    if list(z) != list(zb):  # only a floating-point tie may separate the two
+        assert oracle.energy(model, scene, p, zb) == pytest.approx(E, rel=1e-9)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("block", range(10))
+def test_dp_equals_dfs_brute_C0_1000_seeds(block):
+    for seed in range(block * 100, block * 100 + 100):
+        model, scene, p, _, _ = _c0(seed)
+        E, _, _, z = oracle.match(model, scene, p)
+        Eb, zb, _ = oracle.brute(model, scene, p, prune=True)
+        assert E == pytest.approx(Eb, rel=1e-9), seed
+
+
+# ------------------------------------------------------------- special cases
+def test_zero_dummy_cost_gives_zero_energy():
+    for seed in range(40):
+        model, scene, p = tiny_instance(2000 + seed, M_range=(1, 6), S_range=(1, 10))
+        p["w_dummy"] = 0.0
+        assert oracle.match(model, scene, p)[0] == 0.0
+
+
+def test_single_node_model_is_min_unary():
+    for seed in range(40):
+        model, scene, p = tiny_instance(3000 + seed, M_range=(1, 1), S_range=(1, 12))
+        E, _, _, z = oracle.match(model, scene, p)
+        u = [np.linalg.norm(model.f[0] - scene.f[n]) for n in range(scene.n)] + [p["w_dummy"]]
+        assert E == pytest.approx(p["lambda1"] * min(u), rel=1e-12)
+        k = int(np.argmin(u))
+        assert z[0] == (k if k < scene.n else -1)
+
+
+def _textbook_monotone(model, scene, lam1):
+    """min sum_i lam1 U(i, z_i) over label sequences with strictly increasing
+    scene frames: the O(M S^2) assignment DP of a textbook (no angles, no
+    closeness, no dummy)."""
+    M, S = model.n, scene.n
+    U = np.linalg.norm(model.f[:, None, :] - scene.f[None, :, :], axis=2) * lam1
+    best = U[0].copy()
+    for i in range(1, M):
+        nxt = np.full(S, math.inf)
+        for n in range(S):
+            prev = [best[k] for k in range(S) if scene.t[k] < scene.t[n]]
+            if prev:
+                nxt[n] = U[i, n] + min(prev)
+        best = nxt
+    return best.min()
+
+
+def test_no_geometry_no_dummy_no_closeness_is_monotone_assignment():
+    """lambda2 = 0, W^d -> inf (1e6), T -> inf: the DP reduces to monotone assignment."""
+    for seed in range(40):
+        rng = np.random.default_rng(4000 + seed)
+        M, S = int(rng.integers(1, 6)), int(rng.integers(6, 16))
+        model = NodeSet(np.arange(M, dtype=np.int32), rng.random(M), rng.random(M), rng.random((M, 3)))
+        scene = NodeSet(np.sort(rng.integers(0, 12, S)).astype(np.int32), rng.random(S), rng.random(S),
+                        rng.random((S, 3)))
+        p = dict(lambda1=0.7, lambda2=0.0, lambda3=5.0, w_dummy=1e6, T=10 ** 6)
+        ref = _textbook_monotone(model, scene, 0.7)
+        E = oracle.match(model, scene, p)[0]
+        if math.isfinite(ref):
+            assert E == pytest.approx(ref, rel=1e-12)
+        else:
+            assert E >= 1e6 * 0.7
+
+
+# ---------------------------------------------------------------- invariants
+def _perm_within_frames(scene: NodeSet, rng):
+    idx = np.arange(scene.n)
+    for f in np.unique(scene.t):
+        sel = np.nonzero(scene.t == f)[0]
+        idx[sel] = rng.permutation(sel)
+    return NodeSet(scene.t[idx], scene.x[idx], scene.y[idx], scene.f[idx])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_invariances_bit_identical(seed):
+    """Within-frame relabelling (the north star's label permutation), scene time
+    shift, integer translation, 90-degree rotation and x2 scale leave E* unchanged."""
+    model, scene, p, _, _ = _c0(seed, T=5)
+    E0 = oracle.match(model, scene, p)[0]
+    rng = np.random.default_rng(seed)
+    variants = [
+        _perm_within_frames(scene, rng),
+        NodeSet(scene.t + 17, scene.x, scene.y, scene.f),
+        NodeSet(scene.t, scene.x + 13, scene.y - 7, scene.f),
+        NodeSet(scene.t, -scene.y, scene.x.copy(), scene.f),
+        NodeSet(scene.t, 2 * scene.x, 2 * scene.y, scene.f),
+    ]
+    for v in variants:
+        assert oracle.match(model, v, p)[0] == E0
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_energy_non_increasing_in_T(seed):
+    wl = synth.make_workload("C0", seed=seed, T=5)
+    model = oracle.model_nodes(wl.models[0])
+    _, scene = oracle.scene_nodes(wl.scenes[0])
+    prev = math.inf
+    for T in (1, 2, 3, 5, 8, 10, 40):
+        p = dict(wl.params(), T=T)
+        E = oracle.match(model, scene, p)[0]
+        assert E <= prev + 1e-12
+        prev = E
+
+
+def _ground_truth(wl):
+    """Planted chain labels: the planted copy repeats the model's raw points in
+    order, appended after the 32 clutter points (synth.make_workload C0)."""
+    chain = oracle.model_chain(wl.models[0].frame, wl.models[0].saliency)
+    return 32 + chain  # input ids of the planted chain nodes
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_ground_truth_upper_bounds_optimum(seed):
+    model, scene, p, wl, order = _c0(seed)
+    inv = np.empty_like(order)
+    inv[order] = np.arange(order.size)
+    gt = inv[_ground_truth(wl)]  # sorted-scene labels (window = whole scene)
+    if not oracle.feasible(model, scene, p, gt):
+        pytest.skip("planted copy warped beyond T")
+    E = oracle.match(model, scene, p)[0]
+    assert oracle.energy(model, scene, p, gt) >= E - 1e-12
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_zero_noise_planted_copy_recovered_exactly(seed):
+    """an unwarped, unjittered, noise-free planted copy with integer
+    coordinates has energy 0 and is recovered exactly."""
+    rng = np.random.default_rng(seed)
+    model_pts = synth.gen_model(seed % 6, 12, 2, 16, "zero-noise", seed)
+    clutter = synth.gen_clutter(30, 0, 2.0, 16, rng)
+    planted = synth.gen_planted(model_pts, 5, 10, rng, feat_sigma=0.0, jitter=0, warp=False)
+    scene_pts = synth.concat_points([clutter, planted])
+    model = oracle.model_nodes(model_pts)
+    order, scene = oracle.scene_nodes(scene_pts)
+    p = dict(lambda1=0.6, lambda2=0.2, lambda3=5.0, w_dummy=1.0, T=10)
+    E, Er, A, z = oracle.match(model, scene, p)
+    chain = oracle.model_chain(model_pts.frame, model_pts.saliency)
+    inv = np.empty_like(order)
+    inv[order] = np.arange(order.size)
+    gt = inv[clutter.n + chain]
+    # translation may clip at the frame border; only unclipped copies are exact
+    if not np.allclose(np.diff(scene.x[gt]), np.diff(model.x)) or not np.allclose(np.diff(scene.y[gt]),
+                                                                                    np.diff(model.y)):
+        pytest.skip("planted copy clipped at the frame border")
+    assert E == 0.0 and A == 0.0
+    assert list(z) == list(gt)
+
+
+def test_empty_window_all_dummy():
+    model, scene, p, _, _ = _c0(0)
+    empty = scene.slice(0, 0)
+    E, Er, A, z = oracle.match(model, empty, p)
+    assert E == pytest.approx(p["lambda1"] * model.n * p["w_dummy"], rel=1e-15)
+    assert list(z) == [-1] * model.n
