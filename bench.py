@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""Benchmark: detect_actions over a KTH-shaped synthetic scene (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl hgm|reference] [--workload C3|C1]
+
+One "step" = one pass of the whole hot path over the
+rank's batch: scene index + direction band (a2), model chains (a1), unary
+table (a3), state enumeration + recursion (a4-a5), init search + backtrack +
+appearance distance (a6), per-offset model argmin (a7), and for N > 1 the
+NCCL all_gather of packed per-offset winners.
+
+Workload (weak scaling): every rank owns a C3-shaped slice of one long scene
+-- 25,000 frames per GPU at rho = 4 points/frame (~100k points), one planted
+action per 200 frames, 6 models of M = 30, W = 60, stride 1, T = 10.  The
+scene of N GPUs is N x 25,000 frames; rank r matches offsets
+[r*25000, (r+1)*25000) (its windows reach W-1 frames into the next slice).
+
+`value`  : pairs/s with the inputs resident in HBM (device point arrays).
+`e2e`    : same through the public host API (pinned host inputs copied in,
+           winners and scores copied back, every step).
+The oracle (test infrastructure) is executed only for `cpu_baseline` (rank 0,
+N = 1) and for `--impl reference`.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BASELINE_METRIC = "matched (model, offset) pairs/sec and frames/sec at 1/2/4/8 B200; % ALU roofline"
+ISSUE_SLOTS_PER_CAND = 10.5  # 6 FADD + FMUL + FFMA + MUFU + FFMA + 1/2 FMNMX3
+LANES_PER_CLK = 148 * 4 * 32  # 148 SMs x 4 SMSPs x 32 lanes
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="hgm", choices=["hgm", "reference"])
+    ap.add_argument("--workload", default="C3", choices=["C3", "C1"])
+    ap.add_argument("--frames-per-gpu", type=int, default=25000)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------- workload
+def rank_workload(name, rank, world, frames_per_gpu):
+    import synth
+
+    if name == "C1":  # single GPU only: one model vs one 600-frame clip, all offsets
+        wl = synth.make_workload("C1")
+        return dict(models=wl.models, scene=wl.scenes[0], first=0, count=wl.count[0], window=wl.window,
+                    stride=wl.stride, params=wl.params(), frames=600, desc=dict(
+                        workload="C1: 1 model (M=30) x 600-frame clip, rho=2.5, W=60, stride 1, T=10"))
+    total = frames_per_gpu * world
+    W = 60
+    lo = rank * frames_per_gpu
+    hi = min(lo + frames_per_gpu + W - 1, total)
+    wl = synth.make_workload("C3", n_frames=total, frame_range=(lo, hi))
+    n_off_total = total - W + 1
+    k_end = min(lo + frames_per_gpu, n_off_total)
+    return dict(models=wl.models, scene=wl.scenes[0], first=lo, count=k_end - lo, window=W, stride=1,
+                params=wl.params(), frames=k_end - lo,
+                desc=dict(workload=f"C3: long scene, {frames_per_gpu} frames/GPU (rho=4, ~{4 * frames_per_gpu // 1000}k"
+                                   f" points), 6 models M=30, W=60, stride 1, T=10"))
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                       "-lms", "200", "-i", str(gpu_index)], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in rows for j in range(4) if r[5 + j].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max((float(r[3]) for r in rows if r[3].replace(".", "").isdigit()), default=None)}
+
+
+# --------------------------------------------------------------------- oracle
+def oracle_sample_rate(wl, target_s, seed=0, max_pairs=4096):
+    """Time the CPU oracle (as it stands) on a bounded random sample of pairs."""
+    import oracle
+
+    ncores = os.cpu_count() or 1
+    models = [oracle.model_nodes(m) for m in wl["models"]]
+    order, scene = oracle.scene_nodes(wl["scene"])
+    rng = np.random.default_rng(seed)
+
+    def run(n):
+        ks = rng.integers(0, wl["count"], n)
+        ms = rng.integers(0, len(models), n)
+        wins = [oracle.window_range(scene.t, wl["first"] + int(k) * wl["stride"], wl["window"]) for k in ks]
+        t0 = time.perf_counter()
+        E, _, _, _ = oracle.match_batch(models, scene, wl["params"], ms, [w[0] for w in wins], [w[1] for w in wins],
+                                        ncores)
+        return time.perf_counter() - t0, list(zip(ms.tolist(), ks.tolist())), E
+
+    dt, _, _ = run(ncores)
+    rate = ncores / max(dt, 1e-6)
+    n = int(min(max(ncores, rate * target_s), max_pairs))
+    dt, pairs, E = run(n)
+    return dict(value=n / dt, unit="pairs/s", cores=ncores, kind="oracle", elapsed_s=dt, pairs=pairs, E=E,
+                sample=f"{n} uniformly drawn (model, offset) pairs of rank 0's workload, seed {seed}, "
+                       f"fp64 C oracle, {ncores} threads")
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    wl = rank_workload(args.workload, 0, 1, args.frames_per_gpu)
+    for _ in range(args.warmup):
+        oracle_sample_rate(wl, 1.0, seed=99)
+    vals, secs = [], []
+    for s in range(args.steps):
+        r = oracle_sample_rate(wl, max(2.0, args.cpu_seconds / 2), seed=s)
+        vals.append(r["value"])
+        secs.append(r["elapsed_s"])
+    value = len(vals) / sum(1.0 / v for v in vals)  # harmonic mean = total pairs / total time
+    cpu = dict(value=value, unit="pairs/s", cores=r["cores"], kind="oracle", sample=r["sample"])
+    line = dict(impl="reference", metric=BASELINE_METRIC, value=value, unit="pairs/s", n_gpus=args.gpus,
+                steps=args.steps, warmup=args.warmup, ms_per_step=1000 * sum(secs) / len(secs),
+                higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64", data="synthetic",
+                config=dict(wl["desc"]), cpu_baseline=cpu,
+                e2e=dict(value=value, unit="pairs/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------- own arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    from paper_1505_00581_b200 import hgm
+    from paper_1505_00581_b200.dist import pack_keys  # noqa: F401  (host twin of the device packing)
+    from paper_1505_00581_b200.work import count_work
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    wl = rank_workload(args.workload, rank, world, args.frames_per_gpu)
+    p = wl["params"]
+    n_models = len(wl["models"])
+    count = wl["count"]
+    W, stride, first = wl["window"], wl["stride"], wl["first"]
+
+    # inputs resident in HBM before timing
+    scene_d = hgm.DevicePoints.from_host(wl["scene"], device=dev)
+    models_d = [hgm.DevicePoints.from_host(m, device=dev) for m in wl["models"]]
+    winner = torch.empty(count, dtype=torch.int32, device=dev)
+    score = torch.empty(count, dtype=torch.float32, device=dev)
+    maxn = torch.tensor([count], device=dev)
+    if world > 1:
+        dist.all_reduce(maxn, op=dist.ReduceOp.MAX)
+    keys = torch.empty(int(maxn.item()), dtype=torch.int64, device=dev)
+    gathered = [torch.empty_like(keys) for _ in range(world)]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    def gather(win, sc):
+        if world == 1:
+            return
+        keys.fill_(-1)
+        keys[:count] = (sc.view(torch.int32).to(torch.int64) << 32) | win.to(torch.int64)
+        dist.all_gather(gathered, keys)
+
+    def step():
+        scene = hgm.build_scene_index(scene_d, T_max=p["T"])
+        models = [hgm.build_model_graph(m) for m in models_d]
+        hgm.detect_actions(models, scene, p, first, stride, count, W, out=(winner, score, None))
+        gather(winner, score)
+        return scene, models
+
+    # exact algorithmic work of the recursion (host count from the frame histogram)
+    Ms = []
+    for m in wl["models"]:
+        Ms.append(len(np.unique(m.frame)))
+    wk = count_work(wl["scene"].frame, first, stride, count, W, p["T"])
+    steps_per_pair = sum(max(M - 2, 0) for M in Ms)
+    work_cand = wk.real_candidates * steps_per_pair
+    work_states = (wk.real_states + wk.eps_states) * steps_per_pair
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    hgm.set_profiling(True)
+    hgm.get_stats(reset=True)
+    gpu_idx = local
+    cvd = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if cvd:
+        gpu_idx = cvd.split(",")[local]
+    clocks = ClockSampler(gpu_idx)
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    ev0.record()
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flush between steps (counted inside the timed region)
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    wall = time.perf_counter() - t0
+    ms = ev0.elapsed_time(ev1)
+    ck = clocks.stop()
+    st = hgm.get_stats(reset=True)
+    hgm.set_profiling(False)
+    t = torch.tensor([ms, float(count * n_models), float(wl["frames"])], dtype=torch.float64, device=dev)
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        ms_max, pairs_tot, frames_tot = tmax[0].item(), tsum[1].item(), tsum[2].item()
+    else:
+        ms_max, pairs_tot, frames_tot = ms, float(count * n_models), float(wl["frames"])
+    ms_step = ms_max / args.steps
+    value = pairs_tot / (ms_step / 1000.0)
+    launches = int(sum(st["launches"].values()))
+
+    # roofline of the dominant kernel (K-DP), ALU-bound
+    dp_ms = st["ms"]["dp"] / args.steps
+    f_mhz = ck["sm_mhz"] or 1965.0
+    achieved = work_cand / (dp_ms / 1000.0) / 1e9  # G real-triple candidates / s
+    peak = LANES_PER_CLK * f_mhz * 1e6 / ISSUE_SLOTS_PER_CAND / 1e9
+    roof = dict(bound="alu", achieved=achieved, peak=peak, unit="Gcand/s", frac=achieved / peak, traffic=None,
+                kernel="k_dp_step", dp_ms_per_step=dp_ms, dp_share_of_step=dp_ms / ms_step,
+                candidates_per_step=work_cand, states_per_step=work_states,
+                peak_basis=f"148 SMs x 128 lanes x {f_mhz:.0f} MHz (median SM clock sampled in the timed region)"
+                           f" / {ISSUE_SLOTS_PER_CAND} issue slots per real-triple candidate",
+                kernel_ms={k: v / args.steps for k, v in st["ms"].items()})
+
+    # e2e through the host API: pinned host inputs in, winners + scores out
+    e2e = None
+    if not args.no_e2e:
+        def pin(a):
+            t_ = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+            return t_.numpy()
+
+        class HP:
+            pass
+
+        def pinned(pts):
+            h = HP()
+            h.frame, h.x, h.y, h.saliency, h.feat = (pin(pts.frame), pin(pts.x), pin(pts.y), pin(pts.saliency),
+                                                     pin(pts.feat))
+            h.id = None
+            return h
+
+        sc_h = pinned(wl["scene"])
+        md_h = [pinned(m) for m in wl["models"]]
+        win_h = torch.empty(count, dtype=torch.int32).pin_memory().numpy()
+        sco_h = torch.empty(count, dtype=torch.float32).pin_memory().numpy()
+        h2d = sum(a.nbytes for a in (sc_h.frame, sc_h.x, sc_h.y, sc_h.saliency, sc_h.feat)) + sum(
+            a.nbytes for m in md_h for a in (m.frame, m.x, m.y, m.saliency, m.feat))
+        d2h = win_h.nbytes + sco_h.nbytes
+
+        def step_e2e():
+            scene = hgm.build_scene_index(sc_h, device=local, T_max=p["T"])
+            models = [hgm.build_model_graph(m, device=local) for m in md_h]
+            hgm.detect_actions(models, scene, p, first, stride, count, W, out=(win_h, sco_h, None))
+            if world > 1:
+                gather(torch.from_numpy(win_h).to(dev), torch.from_numpy(sco_h).to(dev))
+                torch.cuda.synchronize()
+            return scene, models
+
+        step_e2e()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ne = max(1, min(args.steps, 3))
+        for _ in range(ne):
+            flush.zero_()
+            step_e2e()
+        e1.record()
+        torch.cuda.synchronize()
+        me = torch.tensor([e0.elapsed_time(e1) / ne], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(me, op=dist.ReduceOp.MAX)
+        e2e = dict(value=pairs_tot / (me.item() / 1000.0), unit="pairs/s", h2d_bytes_per_step=int(h2d),
+                   d2h_bytes_per_step=int(d2h), ms_per_step=me.item(), steps=ne)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = oracle_sample_rate(wl, args.cpu_seconds)
+        # parity spot-check of the timed configuration on the sampled pairs
+        models = [hgm.build_model_graph(m) for m in models_d]
+        scene = hgm.build_scene_index(scene_d, T_max=p["T"])
+        det = hgm.detect_actions(models, scene, p, first, stride, count, W, want_E_all=True)
+        Eg = det.E_all.cpu().numpy()
+        errs = [abs(float(Eg[m, k]) - e) / (1e-6 + 1e-5 * abs(e)) for (m, k), e in zip(r["pairs"], r["E"])]
+        cpu = dict(value=r["value"], unit="pairs/s", cores=r["cores"], kind="oracle", sample=r["sample"],
+                   parity_max_err_over_tol=max(errs) if errs else None)
+
+    if rank == 0:
+        line = dict(metric=BASELINE_METRIC, value=value, unit="pairs/s", n_gpus=world, steps=args.steps,
+                    warmup=args.warmup, ms_per_step=ms_step, higher_is_better=True, scaling="weak",
+                    vs_baseline=None, dtype="f32", data="synthetic",
+                    frames_per_s=frames_tot / (ms_step / 1000.0),
+                    config=dict(wl["desc"], n_models=n_models, offsets_per_gpu=count, pairs_total=int(pairs_tot),
+                                l2="256 MiB buffer written between timed steps (counted)",
+                                parallelism=f"offset-range sharding, {world} rank(s), 1 GPU each"),
+                    roofline=roof, cpu_baseline=cpu, e2e=e2e, clocks=ck, gpu_launches=launches,
+                    wall_s=wall)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,360 @@
+// api.cu -- the extern "C" surface of libhgm.so (include/hgm.h): argument
+// checks, handle ownership, host/device buffer staging, kernel timing.
+// All computation happens in the kernels of scene.cu, unary.cu and dp.cu.
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "hgm_internal.cuh"
+
+namespace hgm {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string &msg) { g_err = msg; }
+hgm_status fail(hgm_status st, const std::string &msg) {
+    g_err = msg;
+    return st;
+}
+hgm_status cuda_fail(cudaError_t e, const char *what) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    cudaGetLastError();  // clear a sticky-free error
+    return e == cudaErrorMemoryAllocation ? HGM_ERR_OUT_OF_MEMORY : HGM_ERR_CUDA;
+}
+
+hgm_status DevBuf::alloc(size_t bytes, cudaStream_t stream) {
+    release();
+    s = stream;
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMallocAsync(&p, bytes, stream);
+    if (e != cudaSuccess) {
+        p = nullptr;
+        return cuda_fail(e, "cudaMallocAsync");
+    }
+    return HGM_OK;
+}
+void DevBuf::release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+}
+
+// ------------------------------------------------------------------ profiling
+namespace {
+std::mutex g_mu;
+bool g_prof = false;
+struct Pending {
+    int cls;
+    cudaEvent_t a, b;
+};
+std::vector<Pending> g_pending;
+hgm_stats g_stats{};
+}  // namespace
+
+bool profiling() { return g_prof; }
+
+Timer::Timer(cudaStream_t s_, int cls_) : s(s_), cls(cls_) {
+    if (!g_prof) return;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
+}
+Timer::~Timer() {
+    if (!a) return;
+    cudaEventRecord(b, s);
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_pending.push_back({cls, a, b});
+}
+
+void count_launch(int cls, int64_t n) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_stats.launches[cls] += n;
+    if (cls == K_DP) g_stats.dp_launches += n;
+}
+
+}  // namespace hgm
+
+using namespace hgm;
+
+// ------------------------------------------------------------------ helpers
+static bool is_device_ptr(const void *p) {
+    if (!p) return false;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+static hgm_status check_points(const hgm_points *pts) {
+    if (!pts) return fail(HGM_ERR_INVALID_ARGUMENT, "points == NULL");
+    if (pts->n <= 0) return fail(HGM_ERR_EMPTY_POINT_SET, "empty point set");
+    if (pts->F < 1) return fail(HGM_ERR_INVALID_ARGUMENT, "descriptor length F < 1");
+    if (!pts->frame || !pts->x || !pts->y || !pts->feat) return fail(HGM_ERR_INVALID_ARGUMENT, "NULL point array");
+    return HGM_OK;
+}
+
+static hgm_status check_params(const hgm_params *p, const hgm_scene *sc) {
+    if (!p) return fail(HGM_ERR_INVALID_ARGUMENT, "params == NULL");
+    const float v[4] = {p->lambda1, p->lambda2, p->lambda3, p->w_dummy};
+    for (float x : v)
+        if (!std::isfinite(x) || x < 0.f) return fail(HGM_ERR_INVALID_ARGUMENT, "lambda / W^d must be finite and >= 0");
+    if (p->T < 1) return fail(HGM_ERR_INVALID_ARGUMENT, "T < 1");
+    if (sc && p->T > sc->T_max) return fail(HGM_ERR_INVALID_ARGUMENT, "T exceeds the scene index T_max");
+    return HGM_OK;
+}
+
+static hgm_status check_offsets(const hgm_offsets *o) {
+    if (!o) return fail(HGM_ERR_INVALID_ARGUMENT, "offsets == NULL");
+    if (o->window < 1 || o->stride < 1 || o->count < 0)
+        return fail(HGM_ERR_INVALID_ARGUMENT, "window < 1, stride < 1 or count < 0");
+    return HGM_OK;
+}
+
+// Copy a host point set to the device (borrowed input, copied per the ABI).
+struct DevPoints {
+    DevBuf frame, x, y, sal, feat, id;
+    hgm_points v{};
+    hgm_status load(const hgm_points *h, cudaStream_t s) {
+        const int64_t n = h->n;
+        HGM_TRY(frame.alloc(sizeof(int32_t) * n, s));
+        HGM_TRY(x.alloc(sizeof(float) * n, s));
+        HGM_TRY(y.alloc(sizeof(float) * n, s));
+        HGM_TRY(sal.alloc(sizeof(float) * n, s));
+        HGM_TRY(feat.alloc(sizeof(float) * n * h->F, s));
+        HGM_CUDA(cudaMemcpyAsync(frame.p, h->frame, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+        HGM_CUDA(cudaMemcpyAsync(x.p, h->x, sizeof(float) * n, cudaMemcpyHostToDevice, s));
+        HGM_CUDA(cudaMemcpyAsync(y.p, h->y, sizeof(float) * n, cudaMemcpyHostToDevice, s));
+        if (h->saliency) {
+            HGM_CUDA(cudaMemcpyAsync(sal.p, h->saliency, sizeof(float) * n, cudaMemcpyHostToDevice, s));
+        } else {
+            HGM_CUDA(cudaMemsetAsync(sal.p, 0, sizeof(float) * n, s));
+        }
+        HGM_CUDA(cudaMemcpyAsync(feat.p, h->feat, sizeof(float) * n * h->F, cudaMemcpyHostToDevice, s));
+        v = *h;
+        v.frame = frame.as<int32_t>();
+        v.x = x.as<float>();
+        v.y = y.as<float>();
+        v.saliency = sal.as<float>();
+        v.feat = feat.as<float>();
+        v.id = nullptr;
+        if (h->id) {
+            HGM_TRY(id.alloc(sizeof(int64_t) * n, s));
+            HGM_CUDA(cudaMemcpyAsync(id.p, h->id, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+            v.id = id.as<int64_t>();
+        }
+        return HGM_OK;
+    }
+};
+
+struct StreamGuard {  // a private stream for the synchronous host-input builders
+    cudaStream_t s = nullptr;
+    ~StreamGuard() {
+        if (s) cudaStreamDestroy(s);
+    }
+};
+
+static inline int host_first(const hgm_scene *sc, int64_t f) {
+    if (f <= 0) return 0;
+    if (f > sc->fmax) return (int)sc->S;
+    return sc->first_h[f];
+}
+
+// ------------------------------------------------------------------ ABI
+extern "C" {
+
+const char *hgm_last_error(void) { return g_err.c_str(); }
+const char *hgm_version(void) { return "hgm 0.1 (sm_100a)"; }
+
+hgm_status hgm_build_model_graph(const hgm_points *pts, int device, hgm_model **out) {
+    HGM_TRY(check_points(pts));
+    if (!out) return fail(HGM_ERR_INVALID_ARGUMENT, "out == NULL");
+    HGM_CUDA(cudaSetDevice(device));
+    StreamGuard sg;
+    HGM_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+    hgm_status st;
+    {
+        DevPoints dp;
+        HGM_TRY(dp.load(pts, sg.s));
+        st = model_build_device(&dp.v, sg.s, out);
+    }
+    HGM_CUDA(cudaStreamSynchronize(sg.s));
+    return st;
+}
+
+hgm_status hgm_build_model_graph_dev(const hgm_points *pts, void *stream, hgm_model **out) {
+    HGM_TRY(check_points(pts));
+    if (!out) return fail(HGM_ERR_INVALID_ARGUMENT, "out == NULL");
+    return model_build_device(pts, (cudaStream_t)stream, out);
+}
+
+hgm_status hgm_model_num_nodes(const hgm_model *m, int32_t *M) {
+    if (!m || !M) return fail(HGM_ERR_INVALID_ARGUMENT, "NULL argument");
+    *M = m->M;
+    return HGM_OK;
+}
+
+void hgm_free_model(hgm_model *m) {
+    if (!m) return;
+    void *ptrs[] = {m->t, m->x, m->y, m->feat, m->step};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    delete m;
+}
+
+hgm_status hgm_build_scene_index(const hgm_points *pts, int device, int32_t T_max, hgm_scene **out) {
+    HGM_TRY(check_points(pts));
+    if (!out) return fail(HGM_ERR_INVALID_ARGUMENT, "out == NULL");
+    if (T_max < 1) return fail(HGM_ERR_INVALID_ARGUMENT, "T_max < 1");
+    HGM_CUDA(cudaSetDevice(device));
+    StreamGuard sg;
+    HGM_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+    hgm_status st;
+    {
+        DevPoints dp;
+        HGM_TRY(dp.load(pts, sg.s));
+        st = scene_build_device(&dp.v, T_max, sg.s, out);
+    }
+    HGM_CUDA(cudaStreamSynchronize(sg.s));
+    return st;
+}
+
+hgm_status hgm_build_scene_index_dev(const hgm_points *pts, int32_t T_max, void *stream, hgm_scene **out) {
+    HGM_TRY(check_points(pts));
+    if (!out) return fail(HGM_ERR_INVALID_ARGUMENT, "out == NULL");
+    if (T_max < 1) return fail(HGM_ERR_INVALID_ARGUMENT, "T_max < 1");
+    return scene_build_device(pts, T_max, (cudaStream_t)stream, out);
+}
+
+hgm_status hgm_scene_num_nodes(const hgm_scene *sc, int64_t *S) {
+    if (!sc || !S) return fail(HGM_ERR_INVALID_ARGUMENT, "NULL argument");
+    *S = sc->S;
+    return HGM_OK;
+}
+
+void hgm_free_scene(hgm_scene *sc) {
+    if (!sc) return;
+    void *ptrs[] = {sc->t, sc->x, sc->y, sc->feat, sc->id, sc->first_tab, sc->qstart, sc->theta, sc->coinc, sc->prow};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    delete sc;
+}
+
+// node range covered by all windows of `o`
+static void covered_range(const hgm_scene *sc, const hgm_offsets *o, int64_t *lo, int64_t *hi) {
+    const int64_t last = (int64_t)o->first_frame + (int64_t)(o->count - 1) * o->stride;
+    *lo = host_first(sc, o->first_frame);
+    *hi = host_first(sc, last + o->window);
+}
+
+hgm_status hgm_match_model_at_offsets(const hgm_model *model, const hgm_scene *scene, const hgm_params *params,
+                                      const hgm_offsets *offsets, float *E, float *A, int64_t *z, void *stream) {
+    if (!model || !scene) return fail(HGM_ERR_INVALID_ARGUMENT, "NULL handle");
+    HGM_TRY(check_params(params, scene));
+    HGM_TRY(check_offsets(offsets));
+    if (model->F != scene->F) return fail(HGM_ERR_DIMENSION_MISMATCH, "model and scene descriptor lengths differ");
+    const int count = offsets->count;
+    if (count == 0) return HGM_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    HGM_CUDA(cudaSetDevice(scene->device));
+    int64_t n_lo, n_hi;
+    covered_range(scene, offsets, &n_lo, &n_hi);
+    const int64_t nn = std::max<int64_t>(n_hi - n_lo, 1);
+    DevBuf U, dE, dA, dz;
+    HGM_TRY(U.alloc(sizeof(float) * (size_t)model->M * nn, s));
+    HGM_TRY(unary_table(model->feat, model->M, model->Fp, scene, n_lo, n_hi, U.as<float>(), s));
+    const bool hE = E && !is_device_ptr(E), hA = A && !is_device_ptr(A), hz = z && !is_device_ptr(z);
+    if (hE) HGM_TRY(dE.alloc(sizeof(float) * count, s));
+    if (hA) HGM_TRY(dA.alloc(sizeof(float) * count, s));
+    if (hz) HGM_TRY(dz.alloc(sizeof(int64_t) * (size_t)count * model->M, s));
+    MatchOut mo{hE ? dE.as<float>() : E, hA ? dA.as<float>() : A, hz ? dz.as<int64_t>() : z};
+    HGM_TRY(match_model(model, scene, *params, *offsets, U.as<float>(), n_lo, nn, mo, s));
+    if (hE) HGM_CUDA(cudaMemcpyAsync(E, dE.p, sizeof(float) * count, cudaMemcpyDeviceToHost, s));
+    if (hA) HGM_CUDA(cudaMemcpyAsync(A, dA.p, sizeof(float) * count, cudaMemcpyDeviceToHost, s));
+    if (hz) HGM_CUDA(cudaMemcpyAsync(z, dz.p, sizeof(int64_t) * count * model->M, cudaMemcpyDeviceToHost, s));
+    if (hE || hA || hz) HGM_CUDA(cudaStreamSynchronize(s));
+    HGM_CUDA(cudaGetLastError());
+    return HGM_OK;
+}
+
+hgm_status hgm_detect_actions(const hgm_model *const *models, int32_t n_models, const hgm_scene *scene,
+                              const hgm_params *params, const hgm_offsets *offsets, int32_t score_mode,
+                              float threshold, int32_t *winner, float *score, float *E_all, void *stream) {
+    if (!models || n_models <= 0) return fail(HGM_ERR_EMPTY_POINT_SET, "empty model dictionary");
+    if (!scene) return fail(HGM_ERR_INVALID_ARGUMENT, "NULL scene");
+    HGM_TRY(check_params(params, scene));
+    HGM_TRY(check_offsets(offsets));
+    if (score_mode != 0 && score_mode != 1) return fail(HGM_ERR_INVALID_ARGUMENT, "score_mode must be 0 or 1");
+    int M_total = 0;
+    for (int m = 0; m < n_models; ++m) {
+        if (!models[m]) return fail(HGM_ERR_INVALID_ARGUMENT, "NULL model handle");
+        if (models[m]->F != scene->F) return fail(HGM_ERR_DIMENSION_MISMATCH, "model and scene descriptor lengths differ");
+        M_total += models[m]->M;
+    }
+    const int count = offsets->count;
+    if (count == 0) return HGM_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    HGM_CUDA(cudaSetDevice(scene->device));
+    int64_t n_lo, n_hi;
+    covered_range(scene, offsets, &n_lo, &n_hi);
+    const int64_t nn = std::max<int64_t>(n_hi - n_lo, 1);
+    const int Fp = scene->Fp;
+    DevBuf mfeat, U, Eb, Ab, zb, wdev, sdev;
+    HGM_TRY(mfeat.alloc(sizeof(float) * (size_t)M_total * Fp, s));
+    int Mmax = 0;
+    for (int m = 0, base = 0; m < n_models; ++m) {
+        HGM_CUDA(cudaMemcpyAsync(mfeat.as<float>() + (size_t)base * Fp, models[m]->feat,
+                                 sizeof(float) * (size_t)models[m]->M * Fp, cudaMemcpyDeviceToDevice, s));
+        base += models[m]->M;
+        Mmax = std::max(Mmax, models[m]->M);
+    }
+    HGM_TRY(U.alloc(sizeof(float) * (size_t)M_total * nn, s));
+    HGM_TRY(unary_table(mfeat.as<float>(), M_total, Fp, scene, n_lo, n_hi, U.as<float>(), s));
+    const bool dEall = E_all && is_device_ptr(E_all);
+    HGM_TRY(Ab.alloc(sizeof(float) * (size_t)n_models * count, s));
+    if (!dEall) HGM_TRY(Eb.alloc(sizeof(float) * (size_t)n_models * count, s));
+    float *Ed = dEall ? E_all : Eb.as<float>();
+    HGM_TRY(zb.alloc(sizeof(int64_t) * (size_t)count * Mmax, s));
+    for (int m = 0, base = 0; m < n_models; ++m) {
+        MatchOut mo{Ed + (size_t)m * count, Ab.as<float>() + (size_t)m * count, zb.as<int64_t>()};
+        HGM_TRY(match_model(models[m], scene, *params, *offsets, U.as<float>() + (size_t)base * nn, n_lo, nn, mo, s));
+        base += models[m]->M;
+    }
+    const bool hw = winner && !is_device_ptr(winner), hs = score && !is_device_ptr(score);
+    if (hw) HGM_TRY(wdev.alloc(sizeof(int32_t) * count, s));
+    if (hs) HGM_TRY(sdev.alloc(sizeof(float) * count, s));
+    HGM_TRY(offset_argmin(score_mode == 0 ? Ed : Ab.as<float>(), n_models, count, threshold,
+                          hw ? wdev.as<int32_t>() : winner, hs ? sdev.as<float>() : score, s));
+    if (hw) HGM_CUDA(cudaMemcpyAsync(winner, wdev.p, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, s));
+    if (hs) HGM_CUDA(cudaMemcpyAsync(score, sdev.p, sizeof(float) * count, cudaMemcpyDeviceToHost, s));
+    if (E_all && !dEall)
+        HGM_CUDA(cudaMemcpyAsync(E_all, Ed, sizeof(float) * (size_t)n_models * count, cudaMemcpyDeviceToHost, s));
+    if (hw || hs || (E_all && !dEall)) HGM_CUDA(cudaStreamSynchronize(s));
+    HGM_CUDA(cudaGetLastError());
+    return HGM_OK;
+}
+
+hgm_status hgm_set_profiling(int enable) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_prof = enable != 0;
+    return HGM_OK;
+}
+
+hgm_status hgm_get_stats(hgm_stats *out, int reset) {
+    if (!out) return fail(HGM_ERR_INVALID_ARGUMENT, "out == NULL");
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto &pe : g_pending) {
+        float ms = 0.f;
+        cudaEventSynchronize(pe.b);
+        cudaEventElapsedTime(&ms, pe.a, pe.b);
+        g_stats.ms[pe.cls] += ms;
+        cudaEventDestroy(pe.a);
+        cudaEventDestroy(pe.b);
+    }
+    g_pending.clear();
+    *out = g_stats;
+    if (reset) g_stats = hgm_stats{};
+    return HGM_OK;
+}
+
+}  // extern "C"

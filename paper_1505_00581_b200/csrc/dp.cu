@@ -1,0 +1,361 @@
+// dp.cu -- K-DP (recursion step), K-BT (init search + backtrack + appearance
+// distance) and K-ARG (per-offset model argmin).
+//
+// The recursion (Eqs. 10-11), with lambdas explicit:
+//   alpha_i(b, a) = min_{c in L(b,a) u {eps}} [ lambda1 U_i(c) + lambda2 D(i; c, b, a)
+//                                              + alpha_{i+1}(c, b) ],  alpha_{M+1} = 0
+// over the pruned candidate range L(b, a) = [minnode(t'(b)+1), minnode(t'(a)+T))
+// (readings R1-R3) and the dummy forms of R5.
+//
+// State storage per (model, offset) instance and step ("layer"), fp32:
+//   [ pair states (b,a) | (b, eps) by b | (eps, a) by a | (eps, eps) ]
+// where pair state (b, a) lives at the band index of the pair (a -> b) minus
+// the band index of the window's first row.  Every layer of
+// every step is kept (alpha history); the argmin beta_i of Eq. 12 is NOT
+// stored: K-BT re-evaluates the candidates of the one state it visits per
+// step with the same arithmetic (hgm_device.cuh) and takes the first
+// candidate equal to the minimum -- exactly the first-strict-minimum rule (R11).
+#include <algorithm>
+#include <cfloat>
+
+#include "hgm_device.cuh"
+#include "hgm_internal.cuh"
+
+namespace hgm {
+
+struct SceneView {
+    const int32_t *__restrict__ t;
+    const int32_t *__restrict__ ft;
+    const int32_t *__restrict__ qstart;
+    const float *__restrict__ theta;
+    const uint8_t *__restrict__ coinc;
+    const int32_t *__restrict__ prow;
+    const int64_t *__restrict__ id;
+    int fmax, S;
+    __device__ __forceinline__ int first(int f) const { return first_at(ft, fmax, S, f); }
+};
+
+struct InstDesc {
+    int32_t wb, we;   // window node range [wb, we)
+    int32_t pbase;    // band index of the window's first row = qstart[wb]
+    int32_t np;       // pair states of the window = qstart[we] - qstart[wb]
+    int64_t off;      // offset of this instance inside a layer
+    int32_t out;      // output slot (offset index)
+    int32_t pad;
+};
+
+struct StepConst {
+    float g_i, g_im1, A1, K2;  // model gaps (Eq. 5) and angle constants (Eq. 6), hgm_device.cuh
+};
+
+struct DPParams {
+    float l1, l2, l23, l1W, W;
+    int T;
+};
+
+__device__ __forceinline__ int ns_of(const InstDesc &d) { return d.np + 2 * (d.we - d.wb) + 1; }
+
+// ------------------------------------------------------------------ K-DP v0
+// One thread per state of one instance; candidates streamed from the band.
+__global__ void __launch_bounds__(256) k_dp_step(SceneView sc, const InstDesc *__restrict__ inst,
+                                                 float *__restrict__ hist, int64_t L, int layer, int has_next,
+                                                 StepConst k, const float *__restrict__ U, int64_t n_lo,
+                                                 DPParams p) {
+    const InstDesc d = inst[blockIdx.y];
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    const int Sw = d.we - d.wb;
+    if (s >= d.np + 2 * Sw + 1) return;
+    float *cur = hist + (int64_t)layer * L + d.off;
+    const float *nxt = has_next ? hist + (int64_t)(layer + 1) * L + d.off : nullptr;
+    const float *Ui = U - n_lo;
+    float out;
+    if (s < d.np) {  // real state (b, a)
+        const int p_ba = d.pbase + s;
+        const int a = sc.prow[p_ba];
+        const int lo_a = sc.first(sc.t[a] + 1);
+        const int b = lo_a + (p_ba - sc.qstart[a]);
+        const int tb = b < sc.S ? sc.t[b] : 0, ta = sc.t[a];
+        if (b >= d.we || tb - ta >= p.T) {
+            cur[s] = INFINITY;  // outside this window / beyond this call's T: never read
+            return;
+        }
+        const int c0 = sc.first(tb + 1);
+        const int c1 = min(sc.first(ta + p.T), d.we);
+        const float th_ab = sc.theta[p_ba];
+        const bool co_ab = sc.coinc[p_ba];
+        int p_bc = sc.qstart[b];              // pair (b -> c), c = c0 + j
+        int p_ac = sc.qstart[a] + (c0 - lo_a); // pair (a -> c)
+        float R = INFINITY;
+        for (int c = c0; c < c1; ++c, ++p_bc, ++p_ac) {
+            const float ncb = msg_n(nxt ? nxt[p_bc - d.pbase] : 0.f, p.l1, Ui[c]);
+            const float m = msg_m(ncb, p.l2, k.g_i, sc.t[c] - tb);
+            const bool cbc = sc.coinc[p_bc];
+            R = fminf(R, cand_value(m, sc.theta[p_bc], th_ab, sc.theta[p_ac], cbc || co_ab, cbc || sc.coinc[p_ac],
+                                   k.A1, k.K2, p.l23));
+        }
+        const float real = __fadd_rn(R, state_const(p.l2, k.g_im1, tb - ta));
+        const float eps = __fadd_rn(p.l1W, nxt ? nxt[d.np + Sw + (b - d.wb)] : 0.f);  // alpha(eps, b)
+        out = fminf(real, eps);
+    } else if (s < d.np + Sw) {  // (b, eps): D = 0 for every candidate (R5)
+        const int b = d.wb + (s - d.np);
+        const int tb = sc.t[b];
+        const int c0 = sc.first(tb + 1), c1 = min(sc.first(tb + p.T), d.we);
+        int p_bc = sc.qstart[b];
+        float R = INFINITY;
+        for (int c = c0; c < c1; ++c, ++p_bc) R = fminf(R, msg_n(nxt ? nxt[p_bc - d.pbase] : 0.f, p.l1, Ui[c]));
+        out = fminf(R, __fadd_rn(p.l1W, nxt ? nxt[d.np + Sw + (b - d.wb)] : 0.f));
+    } else if (s < d.np + 2 * Sw) {  // (eps, a): c constrained by a alone (R5)
+        const int a = d.wb + (s - d.np - Sw);
+        const int ta = sc.t[a];
+        const int c0 = sc.first(ta + 1), c1 = min(sc.first(ta + p.T), d.we);
+        float R = INFINITY;
+        for (int c = c0; c < c1; ++c) R = fminf(R, msg_n(nxt ? nxt[d.np + (c - d.wb)] : 0.f, p.l1, Ui[c]));
+        out = fminf(R, __fadd_rn(p.l1W, nxt ? nxt[d.np + 2 * Sw] : 0.f));
+    } else {  // (eps, eps): unconstrained within the window
+        float R = INFINITY;
+        for (int c = d.wb; c < d.we; ++c) R = fminf(R, msg_n(nxt ? nxt[d.np + (c - d.wb)] : 0.f, p.l1, Ui[c]));
+        out = fminf(R, __fadd_rn(p.l1W, nxt ? nxt[d.np + 2 * Sw] : 0.f));
+    }
+    cur[s] = out;
+}
+
+// ------------------------------------------------------------------ K-BT v0
+// One thread per instance: Eq. 13 init search, Eq. 12 backtrack by
+// re-evaluation, appearance distance.
+struct BTArgs {
+    const float *U;      // U rows of this model's nodes: U[i * nn + (n - n_lo)]
+    int64_t nn, n_lo;
+    const float4 *step;  // model step constants
+    int M;
+    float *E, *A;
+    int64_t *z;          // [count * M]
+};
+
+__global__ void k_backtrack(SceneView sc, const InstDesc *__restrict__ inst, int ninst, const float *__restrict__ hist,
+                            int64_t L, BTArgs bt, DPParams p) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= ninst) return;
+    const InstDesc d = inst[k];
+    const int Sw = d.we - d.wb, EPS = -1, M = bt.M;
+    auto U = [&](int i, int n) { return bt.U[(int64_t)i * bt.nn + (n - bt.n_lo)]; };
+    auto layer = [&](int i) -> const float * {  // alpha_i for 0-based step i (2..M-1); null = alpha == 0
+        return (i >= 2 && i <= M - 1) ? hist + (int64_t)(i - 2) * L + d.off : nullptr;
+    };
+    auto a_pair = [&](const float *l, int later, int earlier) -> float {
+        if (!l) return 0.f;
+        const int lo = sc.first(sc.t[earlier] + 1);
+        return l[sc.qstart[earlier] + (later - lo) - d.pbase];
+    };
+    auto a_be = [&](const float *l, int b) { return l ? l[d.np + (b - d.wb)] : 0.f; };
+    auto a_ea = [&](const float *l, int a) { return l ? l[d.np + Sw + (a - d.wb)] : 0.f; };
+    auto a_ee = [&](const float *l) { return l ? l[d.np + 2 * Sw] : 0.f; };
+
+    // ---- Eq. 13: (z1, z2) = argmin lambda1 U(z1) + lambda1 U(z2) + alpha_3(z2, z1), lexicographic
+    int z1b = EPS, z2b = EPS;
+    float best = INFINITY;
+    if (M == 1) {
+        for (int c = d.wb; c <= d.we; ++c) {
+            const float v = c < d.we ? __fmul_rn(p.l1, U(0, c)) : p.l1W;
+            if (v < best) { best = v; z1b = c < d.we ? c : EPS; }
+        }
+    } else {
+        const float *a3 = layer(2);
+        for (int z1 = d.wb; z1 <= d.we; ++z1) {
+            const bool r1 = z1 < d.we;
+            const float u1 = r1 ? __fmul_rn(p.l1, U(0, z1)) : p.l1W;
+            int c0 = d.wb, c1 = d.we;
+            if (r1) {
+                c0 = sc.first(sc.t[z1] + 1);
+                c1 = min(sc.first(sc.t[z1] + p.T), d.we);
+            }
+            for (int z2 = c0; z2 <= c1; ++z2) {
+                const bool r2 = z2 < c1;
+                const float u2 = r2 ? __fmul_rn(p.l1, U(1, z2)) : p.l1W;
+                float al;
+                if (r1 && r2) al = a_pair(a3, z2, z1);
+                else if (r1) al = a_ea(a3, z1);
+                else if (r2) al = a_be(a3, z2);
+                else al = a_ee(a3);
+                const float v = __fadd_rn(__fadd_rn(u1, u2), al);
+                if (v < best) { best = v; z1b = r1 ? z1 : EPS; z2b = r2 ? z2 : EPS; }
+            }
+        }
+    }
+    int64_t *zo = bt.z ? bt.z + (int64_t)d.out * M : nullptr;
+    float A = z1b == EPS ? p.W : U(0, z1b);
+    if (zo) zo[0] = z1b == EPS ? -1 : sc.id[z1b];
+    if (M >= 2) {
+        A = __fadd_rn(A, z2b == EPS ? p.W : U(1, z2b));
+        if (zo) zo[1] = z2b == EPS ? -1 : sc.id[z2b];
+    }
+    // ---- Eq. 12: z_i = beta_i(z_{i-1}, z_{i-2}), beta re-evaluated
+    int zb = z2b, za = z1b;
+    for (int i = 2; i < M; ++i) {
+        const float *nx = layer(i + 1);
+        const float4 kc = bt.step[i];
+        int zc = EPS;
+        float R = INFINITY;
+        if (zb != EPS && za != EPS) {
+            const int tb = sc.t[zb], ta = sc.t[za];
+            const int lo_a = sc.first(ta + 1);
+            const int c0 = sc.first(tb + 1), c1 = min(sc.first(ta + p.T), d.we);
+            const int p_ba = sc.qstart[za] + (zb - lo_a);
+            const float th_ab = sc.theta[p_ba];
+            const bool co_ab = sc.coinc[p_ba];
+            int arg = EPS;
+            int p_bc = sc.qstart[zb], p_ac = sc.qstart[za] + (c0 - lo_a);
+            for (int c = c0; c < c1; ++c, ++p_bc, ++p_ac) {
+                const float ncb = msg_n(nx ? nx[p_bc - d.pbase] : 0.f, p.l1, U(i, c));
+                const float m = msg_m(ncb, p.l2, kc.x, sc.t[c] - tb);
+                const bool cbc = sc.coinc[p_bc];
+                const float v = cand_value(m, sc.theta[p_bc], th_ab, sc.theta[p_ac], cbc || co_ab,
+                                           cbc || sc.coinc[p_ac], kc.z, kc.w, p.l23);
+                if (v < R) { R = v; arg = c; }
+            }
+            const float real = __fadd_rn(R, state_const(p.l2, kc.y, tb - ta));
+            const float eps = __fadd_rn(p.l1W, a_ea(nx, zb));
+            zc = (real <= eps && arg != EPS) ? arg : EPS;
+        } else if (zb != EPS) {
+            const int tb = sc.t[zb];
+            const int c0 = sc.first(tb + 1), c1 = min(sc.first(tb + p.T), d.we);
+            int arg = EPS, p_bc = sc.qstart[zb];
+            for (int c = c0; c < c1; ++c, ++p_bc) {
+                const float v = msg_n(nx ? nx[p_bc - d.pbase] : 0.f, p.l1, U(i, c));
+                if (v < R) { R = v; arg = c; }
+            }
+            zc = (R <= __fadd_rn(p.l1W, a_ea(nx, zb)) && arg != EPS) ? arg : EPS;
+        } else {
+            int c0 = d.wb, c1 = d.we;
+            if (za != EPS) {
+                c0 = sc.first(sc.t[za] + 1);
+                c1 = min(sc.first(sc.t[za] + p.T), d.we);
+            }
+            int arg = EPS;
+            for (int c = c0; c < c1; ++c) {
+                const float v = msg_n(a_be(nx, c), p.l1, U(i, c));
+                if (v < R) { R = v; arg = c; }
+            }
+            zc = (R <= __fadd_rn(p.l1W, a_ee(nx)) && arg != EPS) ? arg : EPS;
+        }
+        A = __fadd_rn(A, zc == EPS ? p.W : U(i, zc));
+        if (zo) zo[i] = zc == EPS ? -1 : sc.id[zc];
+        za = zb;
+        zb = zc;
+    }
+    if (bt.E) bt.E[d.out] = best;
+    if (bt.A) bt.A[d.out] = A;
+}
+
+// ------------------------------------------------------------------ K-ARG
+// winner(k) = smallest m attaining min_m score(m, k): min over packed keys
+// (float bits << 32 | m); scores are >= 0 so the bit pattern orders like the value.
+__global__ void k_offset_argmin(const float *__restrict__ score, int nm, int count, float thr, int32_t *winner,
+                                float *best) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= count) return;
+    unsigned long long key = ~0ull;
+    for (int m = 0; m < nm; ++m) {
+        const unsigned long long kk =
+            ((unsigned long long)__float_as_uint(score[(int64_t)m * count + k]) << 32) | (unsigned)m;
+        key = kk < key ? kk : key;
+    }
+    const int w = (int)(key & 0xffffffffu);
+    const float v = __uint_as_float((unsigned)(key >> 32));
+    if (winner) winner[k] = v > thr ? -1 : w;
+    if (best) best[k] = v;
+}
+
+hgm_status offset_argmin(const float *score, int n_models, int count, float threshold, int32_t *winner, float *best,
+                         cudaStream_t s) {
+    if (count <= 0) return HGM_OK;
+    Timer tm(s, K_ARG);
+    k_offset_argmin<<<(count + 255) / 256, 256, 0, s>>>(score, n_models, count, threshold, winner, best);
+    count_launch(K_ARG);
+    HGM_CUDA(cudaGetLastError());
+    return HGM_OK;
+}
+
+// ------------------------------------------------------------------ driver
+static inline int host_first(const hgm_scene *sc, int64_t f) {
+    if (f <= 0) return 0;
+    if (f > sc->fmax) return (int)sc->S;
+    return sc->first_h[f];
+}
+
+// Match one model at every offset: K-DP for steps M-1..2 (0-based), then K-BT.
+// U holds this model's rows: U[i * nn + (n - n_lo)].
+hgm_status match_model(const hgm_model *m, const hgm_scene *sc, const hgm_params &pp, const hgm_offsets &o,
+                       const float *U, int64_t n_lo, int64_t nn, MatchOut out, cudaStream_t s) {
+    const int count = o.count, M = m->M;
+    if (count <= 0) return HGM_OK;
+    std::vector<InstDesc> all(count);
+    for (int k = 0; k < count; ++k) {
+        const int64_t of = (int64_t)o.first_frame + (int64_t)k * o.stride;
+        InstDesc d{};
+        d.wb = host_first(sc, of);
+        d.we = host_first(sc, of + o.window);
+        d.pbase = sc->qstart_h[d.wb];
+        d.np = sc->qstart_h[d.we] - sc->qstart_h[d.wb];
+        d.out = k;
+        all[k] = d;
+    }
+    DPParams p;
+    p.l1 = pp.lambda1;
+    p.l2 = pp.lambda2;
+    p.l23 = pp.lambda2 * pp.lambda3;  // one IEEE single multiply
+    p.W = pp.w_dummy;
+    p.l1W = pp.lambda1 * pp.w_dummy;
+    p.T = pp.T;
+    const SceneView v{sc->t, sc->first_tab, sc->qstart, sc->theta, sc->coinc, sc->prow, sc->id, sc->fmax, (int)sc->S};
+    const int nsteps = M >= 3 ? M - 2 : 0;
+    const int64_t budget_floats = (int64_t)1 << 30;  // alpha history per chunk: 4 GiB
+    DevBuf hist, dinst;
+    int64_t hist_cap = 0;
+    HGM_TRY(dinst.alloc(sizeof(InstDesc) * std::min(count, 65535), s));
+    for (int k0 = 0; k0 < count;) {
+        int64_t L = 0;
+        int64_t maxNs = 1;
+        int k1 = k0;
+        while (k1 < count && k1 - k0 < 65535) {
+            InstDesc &d = all[k1];
+            const int64_t ns = (int64_t)d.np + 2 * (int64_t)(d.we - d.wb) + 1;
+            if (k1 > k0 && (L + ns) * std::max(nsteps, 1) > budget_floats) break;
+            d.off = L;
+            L += ns;
+            maxNs = std::max(maxNs, ns);
+            ++k1;
+        }
+        const int ninst = k1 - k0;
+        HGM_CUDA(cudaMemcpyAsync(dinst.p, all.data() + k0, sizeof(InstDesc) * ninst, cudaMemcpyHostToDevice, s));
+        const int64_t need = L * nsteps;
+        if (need > hist_cap) {
+            hist.release();
+            HGM_TRY(hist.alloc(sizeof(float) * need, s));
+            hist_cap = need;
+        }
+        if (nsteps > 0) {
+            Timer tm(s, K_DP);
+            const dim3 grid((unsigned)((maxNs + 255) / 256), (unsigned)ninst);
+            for (int i = M - 1; i >= 2; --i) {
+                const float4 h = m->step_h[i];
+                const StepConst kc{h.x, h.y, h.z, h.w};
+                k_dp_step<<<grid, 256, 0, s>>>(v, dinst.as<InstDesc>(), hist.as<float>(), L, i - 2, i + 1 <= M - 1,
+                                               kc, U + (int64_t)i * nn, n_lo, p);
+            }
+            count_launch(K_DP, nsteps);
+            HGM_CUDA(cudaGetLastError());
+        }
+        {
+            Timer tm(s, K_BT);
+            BTArgs bt{U, nn, n_lo, m->step, M, out.E, out.A, out.z};
+            k_backtrack<<<(ninst + 127) / 128, 128, 0, s>>>(v, dinst.as<InstDesc>(), ninst, hist.as<float>(), L, bt, p);
+            count_launch(K_BT);
+            HGM_CUDA(cudaGetLastError());
+        }
+        // dinst / hist are reused by the next chunk: stream order protects them
+        k0 = k1;
+    }
+    return HGM_OK;
+}
+
+}  // namespace hgm

@@ -1,0 +1,114 @@
+// hgm_internal.cuh -- library-internal types of libhgm.so (not part of the ABI).
+// Data layout in HBM: DESIGN.md §5.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/hgm.h"
+
+namespace hgm {
+
+// ------------------------------------------------------------------ errors
+void set_error(const std::string &msg);
+hgm_status fail(hgm_status st, const std::string &msg);
+hgm_status cuda_fail(cudaError_t e, const char *what);
+
+#define HGM_CUDA(call)                                                   \
+    do {                                                                 \
+        cudaError_t e__ = (call);                                        \
+        if (e__ != cudaSuccess) return ::hgm::cuda_fail(e__, #call);     \
+    } while (0)
+
+#define HGM_TRY(call)                                                    \
+    do {                                                                 \
+        hgm_status s__ = (call);                                         \
+        if (s__ != HGM_OK) return s__;                                   \
+    } while (0)
+
+// Pad descriptors to a multiple of 4 floats so rows load as float4.
+inline int pad4(int F) { return (F + 3) & ~3; }
+
+// RAII device buffer (stream-ordered allocation).
+struct DevBuf {
+    void *p = nullptr;
+    cudaStream_t s = nullptr;
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    ~DevBuf() { release(); }
+    hgm_status alloc(size_t bytes, cudaStream_t stream);
+    void release();
+    template <class T> T *as() const { return static_cast<T *>(p); }
+};
+
+}  // namespace hgm
+
+// ------------------------------------------------------------------ handles
+struct hgm_scene {
+    int device = 0;
+    int64_t S = 0;     // number of scene nodes
+    int F = 0, Fp = 0; // descriptor length, padded length
+    int T_max = 1;     // the band covers frame gaps 1..T_max-1
+    int fmax = 0;      // last occupied frame; first_tab covers frames [0, fmax+1]
+    int64_t npairs = 0;
+    // device (sorted by frame, stable)
+    int32_t *t = nullptr;
+    float *x = nullptr, *y = nullptr;
+    float *feat = nullptr;      // [S * Fp]
+    int64_t *id = nullptr;      // caller ids of the sorted nodes
+    int32_t *first_tab = nullptr; // [fmax + 2]: minnode(f)
+    int32_t *qstart = nullptr;  // [S + 1]: start of row a of the pair band
+    float *theta = nullptr;     // [npairs]: direction of a -> c (K-G)
+    uint8_t *coinc = nullptr;   // [npairs]: 1 if a and c coincide spatially (R10)
+    int32_t *prow = nullptr;    // [npairs]: the earlier node a of each pair
+    // host mirrors (window / chunk sizing without device round-trips)
+    std::vector<int32_t> first_h, qstart_h;
+};
+
+struct hgm_model {
+    int device = 0;
+    int M = 0, F = 0, Fp = 0;
+    int32_t *t = nullptr;
+    float *x = nullptr, *y = nullptr;
+    float *feat = nullptr;  // [M * Fp]
+    float4 *step = nullptr; // [M]: for i >= 2: (g_i, g_{i-1}, A1_i, K2_i), see dp.cu
+    std::vector<int32_t> t_h;
+    std::vector<float4> step_h;  // host mirror: step constants go into launch parameters
+};
+
+namespace hgm {
+
+// ------------------------------------------------------------------ profiling
+enum KClass { K_SCENE = 0, K_MODEL = 1, K_UNARY = 2, K_DP = 3, K_BT = 4, K_ARG = 5 };
+struct Timer {  // CUDA events on the launch stream, only when profiling is on
+    cudaStream_t s;
+    int cls;
+    cudaEvent_t a = nullptr, b = nullptr;
+    Timer(cudaStream_t s_, int cls_);
+    ~Timer();
+};
+void count_launch(int cls, int64_t n = 1);
+bool profiling();
+
+// ------------------------------------------------------------------ launchers
+hgm_status scene_build_device(const hgm_points *dev_pts, int32_t T_max, cudaStream_t s, hgm_scene **out);
+hgm_status model_build_device(const hgm_points *dev_pts, cudaStream_t s, hgm_model **out);
+
+// U[j][n - n_lo] = ||f_j - f'_n|| for j in [0, M_total), n in [n_lo, n_hi)
+hgm_status unary_table(const float *mfeat, int M_total, int Fp, const hgm_scene *sc, int64_t n_lo,
+                       int64_t n_hi, float *U, cudaStream_t s);
+
+struct MatchOut {  // per (model, offset) results of one model
+    float *E;       // [count] device
+    float *A;       // [count] device
+    int64_t *z;     // [count * M] device
+};
+hgm_status match_model(const hgm_model *m, const hgm_scene *sc, const hgm_params &p, const hgm_offsets &o,
+                       const float *U, int64_t n_lo, int64_t nn, MatchOut out, cudaStream_t s);
+hgm_status offset_argmin(const float *score, int n_models, int count, float threshold, int32_t *winner,
+                         float *best, cudaStream_t s);
+
+}  // namespace hgm

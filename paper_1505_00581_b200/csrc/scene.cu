@@ -1,0 +1,290 @@
+// scene.cu -- scene index build and model chain build (a1).
+//
+// Scene (§3.4): stable sort of the points by frame, the
+// minnode table first_tab[f] = first node with frame >= f (R4), and the pair
+// band: for every node a, its successors c in frames (t'(a), t'(a) + T_max),
+// which are the contiguous node range [minnode(t'(a)+1), minnode(t'(a)+T_max)).
+// The band stores the ray direction theta(a->c) (K-G) and a coincidence flag.
+// Every admissible DP state (b, a) is one band entry, and every
+// per-candidate operand of the recursion is a band entry too.
+//
+// Model (§2.1): one most-salient point per occupied frame,
+// ordered by frame, plus per-triple constants of Eqs. 4-6 (gaps, model angles).
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "hgm_device.cuh"
+#include "hgm_internal.cuh"
+
+namespace hgm {
+
+__global__ void k_iota(int32_t *v, int64_t n) {
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < n) v[k] = (int32_t)k;
+}
+
+// gather the sorted nodes; descriptors padded to Fp with zeros
+__global__ void k_gather(int64_t n, int F, int Fp, const int32_t *__restrict__ order, const int32_t *__restrict__ tk,
+                         const float *__restrict__ x, const float *__restrict__ y, const float *__restrict__ feat,
+                         const int64_t *__restrict__ id, int32_t *ot, float *ox, float *oy, float *of, int64_t *oid) {
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    int32_t src = order[k];
+    ot[k] = tk[k];
+    ox[k] = x[src];
+    oy[k] = y[src];
+    if (oid) oid[k] = id ? id[src] : (int64_t)src;
+    const float *fr = feat + (int64_t)src * F;
+    float *fo = of + k * (int64_t)Fp;
+    for (int j = 0; j < Fp; ++j) fo[j] = j < F ? fr[j] : 0.0f;
+}
+
+// first_tab[f] = minnode(f) for f in [0, fmax+1]; each f is written once
+__global__ void k_first_tab(int64_t S, const int32_t *__restrict__ t, int32_t *first_tab) {
+    int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (n > S) return;
+    if (n == S) {
+        first_tab[t[S - 1] + 1] = (int32_t)S;
+        return;
+    }
+    int lo = n == 0 ? 0 : t[n - 1] + 1;
+    for (int f = lo; f <= t[n]; ++f) first_tab[f] = (int32_t)n;
+}
+
+__global__ void k_rowlen(int64_t S, int T_max, int fmax, const int32_t *__restrict__ t,
+                         const int32_t *__restrict__ ft, int32_t *rowlen) {
+    int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (a > S) return;
+    if (a == S) {
+        rowlen[S] = 0;
+        return;
+    }
+    int lo = first_at(ft, fmax, (int)S, t[a] + 1);
+    int hi = first_at(ft, fmax, (int)S, t[a] + T_max);
+    rowlen[a] = hi - lo;
+}
+
+// K-G: direction band theta(a->c) and coincidence flags, one thread per row a
+__global__ void k_band(int64_t S, int T_max, int fmax, const int32_t *__restrict__ t, const float *__restrict__ x,
+                       const float *__restrict__ y, const int32_t *__restrict__ ft, const int32_t *__restrict__ qstart,
+                       float *theta, uint8_t *coinc, int32_t *prow) {
+    int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (a >= S) return;
+    int lo = first_at(ft, fmax, (int)S, t[a] + 1);
+    int hi = first_at(ft, fmax, (int)S, t[a] + T_max);
+    float ax = x[a], ay = y[a];
+    int64_t p = qstart[a];
+    for (int c = lo; c < hi; ++c, ++p) {
+        float cx = x[c], cy = y[c];
+        theta[p] = dir_of(ax, ay, cx, cy);
+        coinc[p] = (ax == cx && ay == cy) ? 1 : 0;
+        prow[p] = (int32_t)a;
+    }
+}
+
+static hgm_status sort_by_frame(const int32_t *frame, int64_t n, int32_t *keys_out, int32_t *order,
+                                cudaStream_t s) {
+    DevBuf iota, tmp;
+    HGM_TRY(iota.alloc(sizeof(int32_t) * n, s));
+    k_iota<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(iota.as<int32_t>(), n);
+    size_t tmp_bytes = 0;
+    HGM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, frame, keys_out, iota.as<int32_t>(), order,
+                                             (int)n, 0, 32, s));
+    HGM_TRY(tmp.alloc(tmp_bytes, s));
+    // radix sort is stable: equal frames keep input order
+    HGM_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, frame, keys_out, iota.as<int32_t>(), order,
+                                             (int)n, 0, 32, s));
+    count_launch(K_SCENE, 2);
+    return HGM_OK;
+}
+
+static void free_scene_dev(hgm_scene *sc) {
+    void *ptrs[] = {sc->t, sc->x, sc->y, sc->feat, sc->id, sc->first_tab, sc->qstart, sc->theta, sc->coinc, sc->prow};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+}
+
+hgm_status scene_build_device(const hgm_points *pts, int32_t T_max, cudaStream_t s, hgm_scene **out) {
+    const int64_t n = pts->n;
+    if (n > (int64_t)INT32_MAX - 1) return fail(HGM_ERR_INVALID_ARGUMENT, "too many scene points");
+    Timer tm(s, K_SCENE);
+    hgm_scene *sc = new hgm_scene();
+    HGM_CUDA(cudaGetDevice(&sc->device));
+    sc->S = n;
+    sc->F = pts->F;
+    sc->Fp = pad4(pts->F);
+    sc->T_max = T_max;
+    auto bail = [&](hgm_status st) {
+        free_scene_dev(sc);
+        delete sc;
+        return st;
+    };
+#define SC_CUDA(call)                                                    \
+    do {                                                                 \
+        cudaError_t e__ = (call);                                        \
+        if (e__ != cudaSuccess) return bail(cuda_fail(e__, #call));      \
+    } while (0)
+    SC_CUDA(cudaMalloc(&sc->t, sizeof(int32_t) * n));
+    SC_CUDA(cudaMalloc(&sc->x, sizeof(float) * n));
+    SC_CUDA(cudaMalloc(&sc->y, sizeof(float) * n));
+    SC_CUDA(cudaMalloc(&sc->feat, sizeof(float) * n * sc->Fp));
+    SC_CUDA(cudaMalloc(&sc->id, sizeof(int64_t) * n));
+    SC_CUDA(cudaMalloc(&sc->qstart, sizeof(int32_t) * (n + 1)));
+    {
+        DevBuf order;
+        if (order.alloc(sizeof(int32_t) * n, s) != HGM_OK) return bail(HGM_ERR_OUT_OF_MEMORY);
+        hgm_status st = sort_by_frame(pts->frame, n, sc->t, order.as<int32_t>(), s);
+        if (st != HGM_OK) return bail(st);
+        unsigned g = (unsigned)((n + 255) / 256);
+        k_gather<<<g, 256, 0, s>>>(n, pts->F, sc->Fp, order.as<int32_t>(), sc->t, pts->x, pts->y, pts->feat, pts->id,
+                                   sc->t, sc->x, sc->y, sc->feat, sc->id);
+        count_launch(K_SCENE);
+        SC_CUDA(cudaGetLastError());
+    }
+    int32_t tt[2];
+    SC_CUDA(cudaMemcpyAsync(&tt[0], sc->t, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SC_CUDA(cudaMemcpyAsync(&tt[1], sc->t + n - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SC_CUDA(cudaStreamSynchronize(s));
+    if (tt[0] < 0) return bail(fail(HGM_ERR_INVALID_ARGUMENT, "negative frame index"));
+    sc->fmax = tt[1];
+    SC_CUDA(cudaMalloc(&sc->first_tab, sizeof(int32_t) * (sc->fmax + 2)));
+    k_first_tab<<<(unsigned)((n + 1 + 255) / 256), 256, 0, s>>>(n, sc->t, sc->first_tab);
+    DevBuf rowlen, tmp;
+    if (rowlen.alloc(sizeof(int32_t) * (n + 1), s) != HGM_OK) return bail(HGM_ERR_OUT_OF_MEMORY);
+    k_rowlen<<<(unsigned)((n + 1 + 255) / 256), 256, 0, s>>>(n, T_max, sc->fmax, sc->t, sc->first_tab,
+                                                             rowlen.as<int32_t>());
+    count_launch(K_SCENE, 2);
+    size_t tb = 0;
+    SC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, rowlen.as<int32_t>(), sc->qstart, (int)(n + 1), s));
+    if (tmp.alloc(tb, s) != HGM_OK) return bail(HGM_ERR_OUT_OF_MEMORY);
+    SC_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, rowlen.as<int32_t>(), sc->qstart, (int)(n + 1), s));
+    count_launch(K_SCENE);
+    sc->first_h.resize(sc->fmax + 2);
+    sc->qstart_h.resize(n + 1);
+    SC_CUDA(cudaMemcpyAsync(sc->first_h.data(), sc->first_tab, sizeof(int32_t) * (sc->fmax + 2),
+                            cudaMemcpyDeviceToHost, s));
+    SC_CUDA(cudaMemcpyAsync(sc->qstart_h.data(), sc->qstart, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, s));
+    SC_CUDA(cudaStreamSynchronize(s));
+    sc->npairs = sc->qstart_h[n];
+    if (sc->npairs > 0) {
+        SC_CUDA(cudaMalloc(&sc->theta, sizeof(float) * sc->npairs));
+        SC_CUDA(cudaMalloc(&sc->coinc, sizeof(uint8_t) * sc->npairs));
+        SC_CUDA(cudaMalloc(&sc->prow, sizeof(int32_t) * sc->npairs));
+        k_band<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(n, T_max, sc->fmax, sc->t, sc->x, sc->y, sc->first_tab,
+                                                           sc->qstart, sc->theta, sc->coinc, sc->prow);
+        count_launch(K_SCENE);
+        SC_CUDA(cudaGetLastError());
+    }
+    SC_CUDA(cudaStreamSynchronize(s));
+#undef SC_CUDA
+    *out = sc;
+    return HGM_OK;
+}
+
+// ------------------------------------------------------------------ model
+// After the stable sort, the first point of each frame run is the earliest
+// input point of that frame; the max-saliency scan with a strict ">" keeps the
+// earliest one on ties (R-D1).
+__global__ void k_model_select(int64_t n, const int32_t *__restrict__ t, const int32_t *__restrict__ order,
+                               const float *__restrict__ sal, int32_t *sel, int32_t *M_out) {
+    // one thread: n is a model's point count (hundreds)
+    if (threadIdx.x == 0) {
+        int m = 0;
+        for (int64_t k = 0; k < n;) {
+            int64_t best = k, j = k + 1;
+            while (j < n && t[j] == t[k]) {
+                if (sal[order[j]] > sal[order[best]]) best = j;
+                ++j;
+            }
+            sel[m++] = (int32_t)best;
+            k = j;
+        }
+        *M_out = m;
+    }
+}
+
+__global__ void k_model_gather(int M, int F, int Fp, const int32_t *__restrict__ sel, const int32_t *__restrict__ t,
+                               const int32_t *__restrict__ order, const float *__restrict__ x,
+                               const float *__restrict__ y, const float *__restrict__ feat, int32_t *ot, float *ox,
+                               float *oy, float *of) {
+    int i = blockIdx.x;
+    if (i >= M) return;
+    int k = sel[i];
+    int src = order[k];
+    if (threadIdx.x == 0) {
+        ot[i] = t[k];
+        ox[i] = x[src];
+        oy[i] = y[src];
+    }
+    for (int j = threadIdx.x; j < Fp; j += blockDim.x) of[(int64_t)i * Fp + j] = j < F ? feat[(int64_t)src * F + j] : 0.f;
+}
+
+// Per-triple model constants for steps i >= 2 (0-based): gaps of Eq. 5 and the
+// model angles of Eq. 6 in the fold representation of hgm_device.cuh.
+__global__ void k_model_steps(int M, const int32_t *__restrict__ t, const float *__restrict__ x,
+                              const float *__restrict__ y, float4 *step) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    if (i < 2) {
+        step[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        return;
+    }
+    int a = i - 2, b = i - 1, c = i;
+    float th_ab = dir_of(x[a], y[a], x[b], y[b]);
+    float th_bc = dir_of(x[b], y[b], x[c], y[c]);
+    float th_ac = dir_of(x[a], y[a], x[c], y[c]);
+    bool co_ab = x[a] == x[b] && y[a] == y[b];
+    bool co_bc = x[b] == x[c] && y[b] == y[c];
+    bool co_ac = x[a] == x[c] && y[a] == y[c];
+    float A1 = (co_bc || co_ab) ? 0.0f : fold(th_bc, th_ab);      // model angle at i-1
+    float K2 = (co_bc || co_ac) ? HGM_PI_F : fold(th_bc, th_ac);  // pi - model angle at i
+    step[i] = make_float4((float)(t[c] - t[b]), (float)(t[b] - t[a]), A1, K2);
+}
+
+hgm_status model_build_device(const hgm_points *pts, cudaStream_t s, hgm_model **out) {
+    const int64_t n = pts->n;
+    if (n > 1000000) return fail(HGM_ERR_INVALID_ARGUMENT, "model point set too large");
+    Timer tm(s, K_MODEL);
+    DevBuf keys, order, sel, Mdev;
+    HGM_TRY(keys.alloc(sizeof(int32_t) * n, s));
+    HGM_TRY(order.alloc(sizeof(int32_t) * n, s));
+    HGM_TRY(sel.alloc(sizeof(int32_t) * n, s));
+    HGM_TRY(Mdev.alloc(sizeof(int32_t), s));
+    HGM_TRY(sort_by_frame(pts->frame, n, keys.as<int32_t>(), order.as<int32_t>(), s));
+    k_model_select<<<1, 32, 0, s>>>(n, keys.as<int32_t>(), order.as<int32_t>(), pts->saliency, sel.as<int32_t>(),
+                                    Mdev.as<int32_t>());
+    count_launch(K_MODEL);
+    int32_t M = 0, t0 = 0;
+    HGM_CUDA(cudaMemcpyAsync(&M, Mdev.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    HGM_CUDA(cudaMemcpyAsync(&t0, keys.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    HGM_CUDA(cudaStreamSynchronize(s));
+    if (t0 < 0) return fail(HGM_ERR_INVALID_ARGUMENT, "negative frame index");
+    hgm_model *m = new hgm_model();
+    HGM_CUDA(cudaGetDevice(&m->device));
+    m->M = M;
+    m->F = pts->F;
+    m->Fp = pad4(pts->F);
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = cudaMalloc(&m->t, sizeof(int32_t) * M);
+    if (e == cudaSuccess) e = cudaMalloc(&m->x, sizeof(float) * M);
+    if (e == cudaSuccess) e = cudaMalloc(&m->y, sizeof(float) * M);
+    if (e == cudaSuccess) e = cudaMalloc(&m->feat, sizeof(float) * M * m->Fp);
+    if (e == cudaSuccess) e = cudaMalloc(&m->step, sizeof(float4) * M);
+    if (e != cudaSuccess) {
+        hgm_free_model(m);
+        return cuda_fail(e, "cudaMalloc(model)");
+    }
+    k_model_gather<<<M, 64, 0, s>>>(M, pts->F, m->Fp, sel.as<int32_t>(), keys.as<int32_t>(), order.as<int32_t>(),
+                                    pts->x, pts->y, pts->feat, m->t, m->x, m->y, m->feat);
+    k_model_steps<<<(M + 63) / 64, 64, 0, s>>>(M, m->t, m->x, m->y, m->step);
+    count_launch(K_MODEL, 2);
+    m->t_h.resize(M);
+    m->step_h.resize(M);
+    HGM_CUDA(cudaMemcpyAsync(m->t_h.data(), m->t, sizeof(int32_t) * M, cudaMemcpyDeviceToHost, s));
+    HGM_CUDA(cudaMemcpyAsync(m->step_h.data(), m->step, sizeof(float4) * M, cudaMemcpyDeviceToHost, s));
+    HGM_CUDA(cudaStreamSynchronize(s));
+    *out = m;
+    return HGM_OK;
+}
+
+}  // namespace hgm

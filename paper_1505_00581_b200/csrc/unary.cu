@@ -1,0 +1,78 @@
+// unary.cu -- K-U: the unary look-up table of PAPER.md §3.3 (L341-366).
+//
+//   U[j][n] = || f_j - f'_n ||_2   (Eq. 2)
+//
+// for every model node j of the call (all models concatenated) and every scene
+// node n of the covered range.  Direct differences with four partial sums in
+// fp32 and a correctly rounded square root.  The GEMM expansion
+// |f|^2 + |f'|^2 - 2 f.f' is NOT used: it cancels for near matches (U ~ 0)
+// and would miss the 1e-6 absolute tolerance, which is also
+// why this is not a tensor-core contraction.
+//
+// Layout: a CTA owns a tile of TN scene nodes and loops over model nodes in
+// tiles of TJ staged in shared memory; each thread keeps its scene node's
+// running partial sums for TJ model nodes in registers while streaming the
+// scene descriptor once per model tile (float4, L1-friendly).
+#include "hgm_internal.cuh"
+
+namespace hgm {
+
+constexpr int KU_TN = 128;  // scene nodes per CTA (one per thread)
+constexpr int KU_TJ = 8;    // model nodes per register tile
+
+__global__ void __launch_bounds__(KU_TN) k_unary(const float *__restrict__ mfeat, int M_total, int Fp,
+                                                 const float *__restrict__ sfeat, int64_t n_lo, int64_t nn,
+                                                 float *__restrict__ U) {
+    extern __shared__ float4 sm[];  // [KU_TJ][Fp/4] model descriptors
+    const int F4 = Fp >> 2;
+    const int64_t n = blockIdx.x * (int64_t)KU_TN + threadIdx.x;
+    const bool live = n < nn;
+    const float4 *srow = reinterpret_cast<const float4 *>(sfeat + (n_lo + (live ? n : 0)) * (int64_t)Fp);
+    for (int j0 = 0; j0 < M_total; j0 += KU_TJ) {
+        const int nj = min(KU_TJ, M_total - j0);
+        __syncthreads();
+        for (int k = threadIdx.x; k < nj * F4; k += KU_TN)
+            sm[k] = reinterpret_cast<const float4 *>(mfeat + (int64_t)j0 * Fp)[k];
+        __syncthreads();
+        float acc[KU_TJ][4];
+#pragma unroll
+        for (int q = 0; q < KU_TJ; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.f;
+        for (int k = 0; k < F4; ++k) {
+            const float4 v = __ldg(srow + k);
+#pragma unroll
+            for (int q = 0; q < KU_TJ; ++q) {
+                if (q < nj) {
+                    const float4 u = sm[q * F4 + k];
+                    float d0 = __fsub_rn(u.x, v.x), d1 = __fsub_rn(u.y, v.y);
+                    float d2 = __fsub_rn(u.z, v.z), d3 = __fsub_rn(u.w, v.w);
+                    acc[q][0] = __fmaf_rn(d0, d0, acc[q][0]);
+                    acc[q][1] = __fmaf_rn(d1, d1, acc[q][1]);
+                    acc[q][2] = __fmaf_rn(d2, d2, acc[q][2]);
+                    acc[q][3] = __fmaf_rn(d3, d3, acc[q][3]);
+                }
+            }
+        }
+        if (live) {
+#pragma unroll
+            for (int q = 0; q < KU_TJ; ++q)
+                if (q < nj)
+                    U[(int64_t)(j0 + q) * nn + n] =
+                        __fsqrt_rn(__fadd_rn(__fadd_rn(acc[q][0], acc[q][1]), __fadd_rn(acc[q][2], acc[q][3])));
+        }
+    }
+}
+
+hgm_status unary_table(const float *mfeat, int M_total, int Fp, const hgm_scene *sc, int64_t n_lo, int64_t n_hi,
+                       float *U, cudaStream_t s) {
+    const int64_t nn = n_hi - n_lo;
+    if (nn <= 0 || M_total <= 0) return HGM_OK;
+    Timer tm(s, K_UNARY);
+    const size_t smem = sizeof(float) * KU_TJ * Fp;
+    if (smem > 48 * 1024) HGM_CUDA(cudaFuncSetAttribute(k_unary, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_unary<<<(unsigned)((nn + KU_TN - 1) / KU_TN), KU_TN, smem, s>>>(mfeat, M_total, Fp, sc->feat, n_lo, nn, U);
+    count_launch(K_UNARY);
+    HGM_CUDA(cudaGetLastError());
+    return HGM_OK;
+}
+
+}  // namespace hgm

@@ -1,0 +1,302 @@
+"""Thin ctypes binding of libhgm.so (include/hgm.h).  Argument marshalling only:
+every step of the matching path runs in the library's CUDA kernels.  There is
+no CPU fallback; if the library or a CUDA device is missing, calls raise.
+
+Names follow the C ABI: build_model_graph, build_scene_index,
+match_model_at_offsets, detect_actions.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libhgm.so")
+
+STATUS = {0: "HGM_OK", 1: "HGM_ERR_EMPTY_POINT_SET", 2: "HGM_ERR_DIMENSION_MISMATCH",
+          3: "HGM_ERR_INVALID_ARGUMENT", 4: "HGM_ERR_OUT_OF_MEMORY", 5: "HGM_ERR_CUDA"}
+
+EXPORTS = ("hgm_build_model_graph", "hgm_build_model_graph_dev", "hgm_model_num_nodes", "hgm_free_model",
+           "hgm_build_scene_index", "hgm_build_scene_index_dev", "hgm_scene_num_nodes", "hgm_free_scene",
+           "hgm_match_model_at_offsets", "hgm_detect_actions", "hgm_set_profiling", "hgm_get_stats",
+           "hgm_last_error", "hgm_version")
+
+
+class HGMError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _Points(C.Structure):
+    _fields_ = [("n", C.c_int64), ("F", C.c_int32), ("frame", C.c_void_p), ("x", C.c_void_p), ("y", C.c_void_p),
+                ("saliency", C.c_void_p), ("feat", C.c_void_p), ("id", C.c_void_p)]
+
+
+class Params(C.Structure):
+    """Energy weights and temporal closeness T."""
+    _fields_ = [("lambda1", C.c_float), ("lambda2", C.c_float), ("lambda3", C.c_float), ("w_dummy", C.c_float),
+                ("T", C.c_int32)]
+
+    @classmethod
+    def make(cls, lambda1=0.6, lambda2=0.2, lambda3=5.0, w_dummy=1.0, T=10):
+        return cls(lambda1, lambda2, lambda3, w_dummy, int(T))
+
+
+class Offsets(C.Structure):
+    _fields_ = [("first_frame", C.c_int32), ("stride", C.c_int32), ("count", C.c_int32), ("window", C.c_int32)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("ms", C.c_double * 6), ("launches", C.c_int64 * 6), ("dp_candidates", C.c_int64),
+                ("dp_states", C.c_int64), ("dp_launches", C.c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libhgm.so; raise loudly if it is missing (no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libhgm.so not built at {LIB_PATH}; run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        vp, P = C.c_void_p, C.POINTER
+        L.hgm_build_model_graph.argtypes = [P(_Points), C.c_int, P(vp)]
+        L.hgm_build_model_graph_dev.argtypes = [P(_Points), vp, P(vp)]
+        L.hgm_model_num_nodes.argtypes = [vp, P(C.c_int32)]
+        L.hgm_free_model.argtypes = [vp]
+        L.hgm_free_model.restype = None
+        L.hgm_build_scene_index.argtypes = [P(_Points), C.c_int, C.c_int32, P(vp)]
+        L.hgm_build_scene_index_dev.argtypes = [P(_Points), C.c_int32, vp, P(vp)]
+        L.hgm_scene_num_nodes.argtypes = [vp, P(C.c_int64)]
+        L.hgm_free_scene.argtypes = [vp]
+        L.hgm_free_scene.restype = None
+        L.hgm_match_model_at_offsets.argtypes = [vp, vp, P(Params), P(Offsets), vp, vp, vp, vp]
+        L.hgm_detect_actions.argtypes = [P(vp), C.c_int32, vp, P(Params), P(Offsets), C.c_int32, C.c_float, vp, vp,
+                                         vp, vp]
+        L.hgm_set_profiling.argtypes = [C.c_int]
+        L.hgm_get_stats.argtypes = [P(Stats), C.c_int]
+        L.hgm_last_error.restype = C.c_char_p
+        L.hgm_version.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(st):
+    if st != 0:
+        raise HGMError(st, lib().hgm_last_error().decode())
+
+
+def _is_torch(a):
+    return type(a).__module__.startswith("torch")
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if _is_torch(a):
+        return a.data_ptr()
+    return a.ctypes.data
+
+
+class _HostPoints:
+    """Contiguous typed host copies of a point set (numpy), kept alive with the struct."""
+
+    def __init__(self, pts):
+        self.frame = np.ascontiguousarray(pts.frame, dtype=np.int32)
+        self.x = np.ascontiguousarray(pts.x, dtype=np.float32)
+        self.y = np.ascontiguousarray(pts.y, dtype=np.float32)
+        sal = getattr(pts, "saliency", None)
+        self.sal = None if sal is None else np.ascontiguousarray(sal, dtype=np.float32)
+        self.feat = np.ascontiguousarray(pts.feat, dtype=np.float32)
+        pid = getattr(pts, "id", None)
+        self.id = None if pid is None else np.ascontiguousarray(pid, dtype=np.int64)
+        n = int(self.frame.shape[0])
+        F = int(self.feat.shape[1]) if self.feat.ndim == 2 else 0
+        self.s = _Points(n, F, _ptr(self.frame), _ptr(self.x), _ptr(self.y), _ptr(self.sal), _ptr(self.feat),
+                         _ptr(self.id))
+
+
+class DevicePoints:
+    """A point set resident in HBM (torch CUDA tensors): frame int32, x/y/saliency
+    float32, feat float32 [n, F] row-major, id int64 or None."""
+
+    def __init__(self, frame, x, y, saliency, feat, id=None):
+        self.frame, self.x, self.y, self.saliency, self.feat, self.id = frame, x, y, saliency, feat, id
+
+    @classmethod
+    def from_host(cls, pts, device="cuda", non_blocking=False, pinned=False):
+        import torch
+
+        def up(a, dt):
+            t = torch.from_numpy(np.ascontiguousarray(a).astype(dt, copy=False))
+            if pinned:
+                t = t.pin_memory()
+            return t.to(device, non_blocking=non_blocking)
+
+        pid = getattr(pts, "id", None)
+        return cls(up(pts.frame, np.int32), up(pts.x, np.float32), up(pts.y, np.float32),
+                   up(pts.saliency, np.float32), up(pts.feat, np.float32), None if pid is None else up(pid, np.int64))
+
+    def cstruct(self):
+        n = int(self.frame.shape[0])
+        F = int(self.feat.shape[1])
+        return _Points(n, F, _ptr(self.frame), _ptr(self.x), _ptr(self.y), _ptr(self.saliency), _ptr(self.feat),
+                       _ptr(self.id))
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        try:
+            import torch
+
+            return torch.cuda.current_stream().cuda_stream
+        except Exception:
+            return None
+    return stream if isinstance(stream, int) else stream.cuda_stream
+
+
+class Model:
+    """Handle of a model chain in HBM (hgm_build_model_graph)."""
+
+    def __init__(self, handle):
+        self.h = C.c_void_p(handle)
+
+    @property
+    def M(self):
+        m = C.c_int32()
+        _check(lib().hgm_model_num_nodes(self.h, C.byref(m)))
+        return m.value
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.h.value and _lib is not None:
+            _lib.hgm_free_model(self.h)
+            self.h = None
+
+
+class Scene:
+    """Handle of a scene index in HBM (hgm_build_scene_index)."""
+
+    def __init__(self, handle, T_max):
+        self.h = C.c_void_p(handle)
+        self.T_max = T_max
+
+    @property
+    def S(self):
+        s = C.c_int64()
+        _check(lib().hgm_scene_num_nodes(self.h, C.byref(s)))
+        return s.value
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.h.value and _lib is not None:
+            _lib.hgm_free_scene(self.h)
+            self.h = None
+
+
+def build_model_graph(points, device: int = 0, stream=None) -> Model:
+    """Model chain: host point sets are copied; DevicePoints stay on the GPU."""
+    out = C.c_void_p()
+    if isinstance(points, DevicePoints):
+        _check(lib().hgm_build_model_graph_dev(C.byref(points.cstruct()), _stream_ptr(stream), C.byref(out)))
+    else:
+        hp = _HostPoints(points)
+        _check(lib().hgm_build_model_graph(C.byref(hp.s), int(device), C.byref(out)))
+    return Model(out.value)
+
+
+def build_scene_index(points, device: int = 0, T_max: int = 10, stream=None) -> Scene:
+    """Scene index."""
+    out = C.c_void_p()
+    if isinstance(points, DevicePoints):
+        _check(lib().hgm_build_scene_index_dev(C.byref(points.cstruct()), int(T_max), _stream_ptr(stream),
+                                               C.byref(out)))
+    else:
+        hp = _HostPoints(points)
+        _check(lib().hgm_build_scene_index(C.byref(hp.s), int(device), int(T_max), C.byref(out)))
+    return Scene(out.value, T_max)
+
+
+def _params(params):
+    if isinstance(params, Params):
+        return params
+    return Params.make(**(params or {}))
+
+
+@dataclass
+class MatchResult:
+    E: object  # [count] float32
+    A: object  # [count] float32
+    z: object  # [count, M] int64 caller ids, -1 = dummy
+
+
+def match_model_at_offsets(model: Model, scene: Scene, params=None, first_frame=0, stride=1, count=1, window=60,
+                           device_out: bool = True, stream=None) -> MatchResult:
+    """E*, A and the assignment of one model at every offset (Eqs. 10-13)."""
+    M = model.M
+    if device_out:
+        import torch
+
+        E = torch.empty(count, dtype=torch.float32, device="cuda")
+        A = torch.empty(count, dtype=torch.float32, device="cuda")
+        z = torch.empty((count, M), dtype=torch.int64, device="cuda")
+    else:
+        E = np.empty(count, np.float32)
+        A = np.empty(count, np.float32)
+        z = np.empty((count, M), np.int64)
+    o = Offsets(int(first_frame), int(stride), int(count), int(window))
+    _check(lib().hgm_match_model_at_offsets(model.h, scene.h, C.byref(_params(params)), C.byref(o), _ptr(E), _ptr(A),
+                                            _ptr(z), _stream_ptr(stream)))
+    return MatchResult(E, A, z)
+
+
+@dataclass
+class DetectResult:
+    winner: object  # [count] int32, -1 above threshold
+    score: object  # [count] float32
+    E_all: object  # [n_models, count] float32 or None
+
+
+def detect_actions(models, scene: Scene, params=None, first_frame=0, stride=1, count=1, window=60, score_mode=0,
+                   threshold=math.inf, want_E_all=False, device_out=True, out=None, stream=None) -> DetectResult:
+    """Per-offset nearest-model detection.  `out` may supply
+    preallocated (winner, score, E_all) buffers."""
+    nm = len(models)
+    if out is not None:
+        winner, score, E_all = out
+    elif device_out:
+        import torch
+
+        winner = torch.empty(count, dtype=torch.int32, device="cuda")
+        score = torch.empty(count, dtype=torch.float32, device="cuda")
+        E_all = torch.empty((nm, count), dtype=torch.float32, device="cuda") if want_E_all else None
+    else:
+        winner = np.empty(count, np.int32)
+        score = np.empty(count, np.float32)
+        E_all = np.empty((nm, count), np.float32) if want_E_all else None
+    handles = (C.c_void_p * nm)(*[m.h.value for m in models])
+    o = Offsets(int(first_frame), int(stride), int(count), int(window))
+    _check(lib().hgm_detect_actions(handles, nm, scene.h, C.byref(_params(params)), C.byref(o), int(score_mode),
+                                    float(threshold), _ptr(winner), _ptr(score), _ptr(E_all), _stream_ptr(stream)))
+    return DetectResult(winner, score, E_all)
+
+
+def set_profiling(enable: bool = True):
+    _check(lib().hgm_set_profiling(int(bool(enable))))
+
+
+def get_stats(reset: bool = False) -> dict:
+    s = Stats()
+    _check(lib().hgm_get_stats(C.byref(s), int(bool(reset))))
+    names = ("scene", "model", "unary", "dp", "backtrack", "argmin")
+    return dict(ms={n: s.ms[i] for i, n in enumerate(names)},
+                launches={n: s.launches[i] for i, n in enumerate(names)}, dp_launches=s.dp_launches)
+
+
+def version() -> str:
+    return lib().hgm_version().decode()

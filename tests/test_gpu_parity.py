@@ -1,0 +1,211 @@
+"""GPU parity: libhgm.so (through the C ABI) against the fp64 CPU oracle on the
+same seeded inputs.  Marked gpu: runs on a B200 only."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests._parity import Checker, tol
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def hgm():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1505_00581_b200 import hgm as H
+
+    H.lib()
+    return H
+
+
+def _run_and_check(H, wl, scene_idx=0, ks=None, max_ties=0.01, models=None):
+    p = wl.params()
+    scene_pts = wl.scenes[scene_idx]
+    count = wl.count[scene_idx]
+    chk = Checker(wl.models, scene_pts, p, wl.first[scene_idx], wl.stride, wl.window)
+    scene = H.build_scene_index(scene_pts, device=0, T_max=p["T"])
+    mids = range(len(wl.models)) if models is None else models
+    ks = list(range(count)) if ks is None else list(ks)
+    pairs = [(m, k) for m in mids for k in ks]
+    E_o, _, A_o, z_o = chk.oracle_pairs(pairs)
+    gpu = {}
+    for m in mids:
+        mh = H.build_model_graph(wl.models[m], device=0)
+        r = H.match_model_at_offsets(mh, scene, p, wl.first[scene_idx], wl.stride, count, wl.window,
+                                     device_out=False)
+        gpu[m] = r
+    bad, ties = [], 0
+    for j, (m, k) in enumerate(pairs):
+        r = gpu[m]
+        msg = chk.check_pair(m, k, r.E[k], r.A[k], r.z[k], E_o[j], A_o[j], z_o[j])
+        if msg == "TIE":
+            ties += 1
+        elif msg:
+            bad.append(msg)
+    assert not bad, bad[:5]
+    assert ties <= max(1, max_ties * len(pairs)), f"{ties} near-ties of {len(pairs)}"
+    return len(pairs), ties
+
+
+@pytest.mark.parametrize("block", range(5))
+def test_c0_seeds(hgm, block):
+    """C0 tiny (M=8, ~40 points, T=5): 200 seeds per block."""
+    for seed in range(block * 200, block * 200 + 200):
+        wl = synth.make_workload("C0", seed=seed)
+        _run_and_check(hgm, wl, max_ties=1.0)
+
+
+def test_c0_T10(hgm):
+    for seed in range(100):
+        wl = synth.make_workload("C0", seed=seed, T=10)
+        _run_and_check(hgm, wl, max_ties=1.0)
+
+
+def test_c1_all_offsets(hgm):
+    """C1: one M=30 model against a 600-frame clip, all 541 offsets."""
+    n, ties = _run_and_check(hgm, synth.make_workload("C1"))
+    assert n == 541
+
+
+def test_c2_sampled(hgm):
+    wl = synth.make_workload("C2")
+    rng = np.random.default_rng(2)
+    for clip in rng.choice(25, 3, replace=False):
+        ks = np.sort(rng.choice(wl.count[clip], 40, replace=False))
+        _run_and_check(hgm, wl, scene_idx=int(clip), ks=ks)
+
+
+def test_c3_sampled_short(hgm):
+    wl = synth.make_workload("C3", n_frames=3000)
+    rng = np.random.default_rng(3)
+    ks = np.sort(rng.choice(wl.count[0], 60, replace=False))
+    _run_and_check(hgm, wl, ks=ks)
+
+
+def test_c4_sampled(hgm):
+    wl = synth.make_workload("C4", T=10, n_frames=1200)
+    _run_and_check(hgm, wl, ks=[0, 40], models=[0, 3])
+
+
+def test_detect_matches_oracle(hgm):
+    """detect_actions winners bit-exact against the oracle (ties: near-tie rule)."""
+    wl = synth.make_workload("C2")
+    clip = 4
+    p = wl.params()
+    count = 120
+    ref = oracle.detect(wl.models, wl.scenes[clip], p, 0, 1, count, wl.window)
+    scene = hgm.build_scene_index(wl.scenes[clip], device=0, T_max=10)
+    models = [hgm.build_model_graph(m, device=0) for m in wl.models]
+    det = hgm.detect_actions(models, scene, p, 0, 1, count, wl.window, want_E_all=True, device_out=False)
+    for k in range(count):
+        E_ref = ref.E[:, k]
+        assert np.all(np.abs(det.E_all[:, k] - E_ref) <= 1e-6 + 1e-5 * np.abs(E_ref)), k
+        w = int(det.winner[k])
+        if w != int(ref.winner[k]):  # accept only a near-tie between the two winners
+            assert abs(E_ref[w] - E_ref[ref.winner[k]]) <= tol(E_ref[ref.winner[k]]), k
+        assert abs(float(det.score[k]) - ref.score[k]) <= tol(ref.score[k])
+
+
+def test_detect_appearance_score_and_threshold(hgm):
+    wl = synth.make_workload("C1")
+    p = wl.params()
+    scene = hgm.build_scene_index(wl.scenes[0], device=0, T_max=10)
+    models = [hgm.build_model_graph(wl.models[0], device=0)]
+    r = hgm.match_model_at_offsets(models[0], scene, p, 0, 1, 50, 60, device_out=False)
+    det = hgm.detect_actions(models, scene, p, 0, 1, 50, 60, score_mode=1, threshold=float(np.median(r.A)),
+                             device_out=False)
+    assert np.array_equal(det.score, r.A)
+    assert np.array_equal(det.winner, np.where(r.A > np.median(r.A), -1, 0))
+
+
+def test_edge_cases(hgm):
+    """Windows past the end, empty windows, M=1, M=2, T=1, coincident points."""
+    p = dict(lambda1=0.6, lambda2=0.2, lambda3=5.0, w_dummy=1.0, T=5)
+    rng = np.random.default_rng(7)
+    for M in (1, 2, 3):
+        wl = synth.make_workload("C0", seed=M)
+        model_pts = wl.models[0].take(np.arange(M))
+        scene_pts = wl.scenes[0]
+        chk = Checker([model_pts], scene_pts, p, -10, 3, 8)
+        scene = hgm.build_scene_index(scene_pts, device=0, T_max=5)
+        mh = hgm.build_model_graph(model_pts, device=0)
+        count = 15  # windows from frame -10 to past the last frame (20)
+        r = hgm.match_model_at_offsets(mh, scene, p, -10, 3, count, 8, device_out=False)
+        pairs = [(0, k) for k in range(count)]
+        E_o, _, A_o, z_o = chk.oracle_pairs(pairs)
+        for j, (m, k) in enumerate(pairs):
+            msg = chk.check_pair(m, k, r.E[k], r.A[k], r.z[k], E_o[j], A_o[j], z_o[j])
+            assert msg in (None, "TIE"), msg
+        # empty windows: all dummies, E = lambda1 M W^d
+        assert math.isclose(float(r.E[0]), 0.6 * M * 1.0, rel_tol=1e-6)
+        assert list(r.z[0]) == [-1] * M
+    # coincident points and T = 1
+    pts = synth.gen_clutter(12, 0, 3.0, 4, rng)
+    pts.x[:] = np.round(pts.x / 40) * 40  # many spatial coincidences
+    pts.y[:] = np.round(pts.y / 40) * 40
+    model_pts = synth.gen_model(1, 6, 1, 4, "edge", 0, gap2_prob=0.0)
+    model_pts.x[:] = np.round(model_pts.x / 40) * 40
+    model_pts.y[:] = np.round(model_pts.y / 40) * 40
+    for T in (1, 2, 4):
+        pp = dict(p, T=T)
+        chk = Checker([model_pts], pts, pp, 0, 1, 12)
+        scene = hgm.build_scene_index(pts, device=0, T_max=4)
+        mh = hgm.build_model_graph(model_pts, device=0)
+        r = hgm.match_model_at_offsets(mh, scene, pp, 0, 1, 1, 12, device_out=False)
+        E_o, _, A_o, z_o = chk.oracle_pairs([(0, 0)])
+        msg = chk.check_pair(0, 0, r.E[0], r.A[0], r.z[0], E_o[0], A_o[0], z_o[0])
+        assert msg in (None, "TIE"), msg
+
+
+def test_errors(hgm):
+    wl = synth.make_workload("C0", seed=0)
+    scene = hgm.build_scene_index(wl.scenes[0], device=0, T_max=5)
+    model = hgm.build_model_graph(wl.models[0], device=0)
+    with pytest.raises(hgm.HGMError) as e:
+        hgm.match_model_at_offsets(model, scene, dict(T=6), 0, 1, 1, 20)
+    assert e.value.status == 3  # T > T_max
+    with pytest.raises(hgm.HGMError) as e:
+        hgm.match_model_at_offsets(model, scene, dict(lambda1=-1.0, T=5), 0, 1, 1, 20)
+    assert e.value.status == 3
+    with pytest.raises(hgm.HGMError) as e:
+        hgm.detect_actions([], scene, dict(T=5), 0, 1, 1, 20)
+    assert e.value.status == 1
+    other = synth.make_workload("C1")
+    m2 = hgm.build_model_graph(other.models[0], device=0)  # F = 162 vs scene F = 8
+    with pytest.raises(hgm.HGMError) as e:
+        hgm.detect_actions([m2], scene, dict(T=5), 0, 1, 1, 20)
+    assert e.value.status == 2
+
+
+def test_device_builders_match_host_builders(hgm):
+    import torch
+
+    wl = synth.make_workload("C1")
+    p = wl.params()
+    s_h = hgm.build_scene_index(wl.scenes[0], device=0, T_max=10)
+    m_h = hgm.build_model_graph(wl.models[0], device=0)
+    s_d = hgm.build_scene_index(hgm.DevicePoints.from_host(wl.scenes[0]), T_max=10)
+    m_d = hgm.build_model_graph(hgm.DevicePoints.from_host(wl.models[0]))
+    a = hgm.match_model_at_offsets(m_h, s_h, p, 0, 1, 100, 60)
+    b = hgm.match_model_at_offsets(m_d, s_d, p, 0, 1, 100, 60)
+    torch.cuda.synchronize()
+    assert torch.equal(a.E, b.E) and torch.equal(a.z, b.z)
+
+
+def test_bit_determinism(hgm):
+    import torch
+
+    wl = synth.make_workload("C1")
+    p = wl.params()
+    s = hgm.build_scene_index(wl.scenes[0], device=0, T_max=10)
+    m = hgm.build_model_graph(wl.models[0], device=0)
+    a = hgm.match_model_at_offsets(m, s, p, 0, 1, 541, 60)
+    b = hgm.match_model_at_offsets(m, s, p, 0, 1, 541, 60)
+    torch.cuda.synchronize()
+    assert torch.equal(a.E, b.E) and torch.equal(a.A, b.A) and torch.equal(a.z, b.z)
