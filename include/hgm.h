@@ -117,13 +117,13 @@ hgm_status hgm_detect_actions(const hgm_model *const *models, int32_t n_models, 
 
 /* Kernel timing (CUDA events on the launch stream) for the roofline report.
  * When enabled, every call accumulates per-kernel-class device time.
- * Classes: 0 scene index, 1 model graph, 2 unary table (K-U), 3 DP steps
- * (K-DP), 4 backtrack (K-BT), 5 offset argmin (K-ARG).  Also counts launches
- * of the library's own kernels and the number of real-triple candidates and
- * states evaluated by K-DP (computed on the host from the frame index). */
+ * Classes: 0 scene index (incl. K-G), 1 model graph, 2 unary table (K-U),
+ * 3 recursion real states (K-DP), 4 backtrack (K-BT), 5 offset argmin (K-ARG),
+ * 6 messages + dummy-form states (K-MSG), 7 reserved.  Also counts launches of
+ * the library's own kernels (dp_launches = K-DP launches). */
 typedef struct {
-    double ms[6];
-    int64_t launches[6];
+    double ms[8];
+    int64_t launches[8];
     int64_t dp_candidates, dp_states, dp_launches;
 } hgm_stats;
 hgm_status hgm_set_profiling(int enable);

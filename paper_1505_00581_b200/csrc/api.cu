@@ -73,6 +73,48 @@ void count_launch(int cls, int64_t n) {
 
 }  // namespace hgm
 
+// ------------------------------------------------------------------ handle lifetime
+static cudaStream_t free_stream(int device) {
+    static std::mutex mu;
+    static cudaStream_t fs[64] = {};
+    std::lock_guard<std::mutex> lk(mu);
+    if (device < 0 || device >= 64) return nullptr;
+    if (!fs[device]) cudaStreamCreateWithFlags(&fs[device], cudaStreamNonBlocking);
+    return fs[device];
+}
+
+void HandleUses::record(cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto &pr : ev)
+        if (pr.first == s) {
+            cudaEventRecord(pr.second, s);
+            return;
+        }
+    cudaEvent_t e;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return;
+    cudaEventRecord(e, s);
+    ev.emplace_back(s, e);
+}
+
+void HandleUses::release_after(const std::vector<void *> &ptrs, int device) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    cudaStream_t fs = free_stream(device);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (auto &pr : ev) {
+            cudaStreamWaitEvent(fs, pr.second, 0);  // after every call that used the handle
+            cudaEventDestroy(pr.second);
+        }
+        ev.clear();
+    }
+    for (void *p : ptrs)
+        if (p) cudaFreeAsync(p, fs);
+    cudaGetLastError();
+    cudaSetDevice(prev);
+}
+
 using namespace hgm;
 
 // ------------------------------------------------------------------ helpers
@@ -154,6 +196,25 @@ struct StreamGuard {  // a private stream for the synchronous host-input builder
     }
 };
 
+// Keep freed stream-ordered allocations in the device pool (no release to the
+// OS at synchronisation points): the per-call scratch (unary table, alpha
+// history, up to a few GB) is then recycled instead of re-mapped every call.
+static void configure_pool() {
+    static std::mutex mu;
+    static bool done[64] = {false};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    done[dev] = true;
+}
+
 static inline int host_first(const hgm_scene *sc, int64_t f) {
     if (f <= 0) return 0;
     if (f > sc->fmax) return (int)sc->S;
@@ -170,6 +231,7 @@ hgm_status hgm_build_model_graph(const hgm_points *pts, int device, hgm_model **
     HGM_TRY(check_points(pts));
     if (!out) return fail(HGM_ERR_INVALID_ARGUMENT, "out == NULL");
     HGM_CUDA(cudaSetDevice(device));
+    configure_pool();
     StreamGuard sg;
     HGM_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
     hgm_status st;
@@ -185,6 +247,7 @@ hgm_status hgm_build_model_graph(const hgm_points *pts, int device, hgm_model **
 hgm_status hgm_build_model_graph_dev(const hgm_points *pts, void *stream, hgm_model **out) {
     HGM_TRY(check_points(pts));
     if (!out) return fail(HGM_ERR_INVALID_ARGUMENT, "out == NULL");
+    configure_pool();
     return model_build_device(pts, (cudaStream_t)stream, out);
 }
 
@@ -196,9 +259,7 @@ hgm_status hgm_model_num_nodes(const hgm_model *m, int32_t *M) {
 
 void hgm_free_model(hgm_model *m) {
     if (!m) return;
-    void *ptrs[] = {m->t, m->x, m->y, m->feat, m->step};
-    for (void *p : ptrs)
-        if (p) cudaFree(p);
+    m->uses.release_after({m->t, m->x, m->y, m->feat, m->step}, m->device);
     delete m;
 }
 
@@ -207,6 +268,7 @@ hgm_status hgm_build_scene_index(const hgm_points *pts, int device, int32_t T_ma
     if (!out) return fail(HGM_ERR_INVALID_ARGUMENT, "out == NULL");
     if (T_max < 1) return fail(HGM_ERR_INVALID_ARGUMENT, "T_max < 1");
     HGM_CUDA(cudaSetDevice(device));
+    configure_pool();
     StreamGuard sg;
     HGM_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
     hgm_status st;
@@ -223,6 +285,7 @@ hgm_status hgm_build_scene_index_dev(const hgm_points *pts, int32_t T_max, void 
     HGM_TRY(check_points(pts));
     if (!out) return fail(HGM_ERR_INVALID_ARGUMENT, "out == NULL");
     if (T_max < 1) return fail(HGM_ERR_INVALID_ARGUMENT, "T_max < 1");
+    configure_pool();
     return scene_build_device(pts, T_max, (cudaStream_t)stream, out);
 }
 
@@ -234,9 +297,9 @@ hgm_status hgm_scene_num_nodes(const hgm_scene *sc, int64_t *S) {
 
 void hgm_free_scene(hgm_scene *sc) {
     if (!sc) return;
-    void *ptrs[] = {sc->t, sc->x, sc->y, sc->feat, sc->id, sc->first_tab, sc->qstart, sc->theta, sc->coinc, sc->prow};
-    for (void *p : ptrs)
-        if (p) cudaFree(p);
+    sc->uses.release_after({sc->t, sc->x, sc->y, sc->feat, sc->id, sc->first_tab, sc->qstart, sc->theta, sc->coinc,
+                            sc->cpre, sc->prow, sc->qpad, sc->theta_pad, sc->rfc, sc->rlc},
+                           sc->device);
     delete sc;
 }
 
@@ -257,18 +320,21 @@ hgm_status hgm_match_model_at_offsets(const hgm_model *model, const hgm_scene *s
     if (count == 0) return HGM_OK;
     cudaStream_t s = (cudaStream_t)stream;
     HGM_CUDA(cudaSetDevice(scene->device));
+    configure_pool();
     int64_t n_lo, n_hi;
     covered_range(scene, offsets, &n_lo, &n_hi);
     const int64_t nn = std::max<int64_t>(n_hi - n_lo, 1);
     DevBuf U, dE, dA, dz;
     HGM_TRY(U.alloc(sizeof(float) * (size_t)model->M * nn, s));
-    HGM_TRY(unary_table(model->feat, model->M, model->Fp, scene, n_lo, n_hi, U.as<float>(), s));
+    HGM_TRY(unary_table(model->feat, model->M, 1, model->Fp, scene, n_lo, n_hi, U.as<float>(), s));
     const bool hE = E && !is_device_ptr(E), hA = A && !is_device_ptr(A), hz = z && !is_device_ptr(z);
     if (hE) HGM_TRY(dE.alloc(sizeof(float) * count, s));
     if (hA) HGM_TRY(dA.alloc(sizeof(float) * count, s));
     if (hz) HGM_TRY(dz.alloc(sizeof(int64_t) * (size_t)count * model->M, s));
     MatchOut mo{hE ? dE.as<float>() : E, hA ? dA.as<float>() : A, hz ? dz.as<int64_t>() : z};
-    HGM_TRY(match_model(model, scene, *params, *offsets, U.as<float>(), n_lo, nn, mo, s));
+    HGM_TRY(match_batch(&model, 1, scene, *params, *offsets, U.as<float>(), n_lo, nn, &mo, s));
+    scene->uses.record(s);
+    model->uses.record(s);
     if (hE) HGM_CUDA(cudaMemcpyAsync(E, dE.p, sizeof(float) * count, cudaMemcpyDeviceToHost, s));
     if (hA) HGM_CUDA(cudaMemcpyAsync(A, dA.p, sizeof(float) * count, cudaMemcpyDeviceToHost, s));
     if (hz) HGM_CUDA(cudaMemcpyAsync(z, dz.p, sizeof(int64_t) * count * model->M, cudaMemcpyDeviceToHost, s));
@@ -295,31 +361,41 @@ hgm_status hgm_detect_actions(const hgm_model *const *models, int32_t n_models, 
     if (count == 0) return HGM_OK;
     cudaStream_t s = (cudaStream_t)stream;
     HGM_CUDA(cudaSetDevice(scene->device));
+    configure_pool();
     int64_t n_lo, n_hi;
     covered_range(scene, offsets, &n_lo, &n_hi);
     const int64_t nn = std::max<int64_t>(n_hi - n_lo, 1);
     const int Fp = scene->Fp;
     DevBuf mfeat, U, Eb, Ab, zb, wdev, sdev;
-    HGM_TRY(mfeat.alloc(sizeof(float) * (size_t)M_total * Fp, s));
     int Mmax = 0;
-    for (int m = 0, base = 0; m < n_models; ++m) {
-        HGM_CUDA(cudaMemcpyAsync(mfeat.as<float>() + (size_t)base * Fp, models[m]->feat,
-                                 sizeof(float) * (size_t)models[m]->M * Fp, cudaMemcpyDeviceToDevice, s));
-        base += models[m]->M;
-        Mmax = std::max(Mmax, models[m]->M);
-    }
-    HGM_TRY(U.alloc(sizeof(float) * (size_t)M_total * nn, s));
-    HGM_TRY(unary_table(mfeat.as<float>(), M_total, Fp, scene, n_lo, n_hi, U.as<float>(), s));
+    for (int m = 0; m < n_models; ++m) Mmax = std::max(Mmax, models[m]->M);
+    (void)M_total;
     const bool dEall = E_all && is_device_ptr(E_all);
     HGM_TRY(Ab.alloc(sizeof(float) * (size_t)n_models * count, s));
     if (!dEall) HGM_TRY(Eb.alloc(sizeof(float) * (size_t)n_models * count, s));
     float *Ed = dEall ? E_all : Eb.as<float>();
-    HGM_TRY(zb.alloc(sizeof(int64_t) * (size_t)count * Mmax, s));
-    for (int m = 0, base = 0; m < n_models; ++m) {
-        MatchOut mo{Ed + (size_t)m * count, Ab.as<float>() + (size_t)m * count, zb.as<int64_t>()};
-        HGM_TRY(match_model(models[m], scene, *params, *offsets, U.as<float>() + (size_t)base * nn, n_lo, nn, mo, s));
-        base += models[m]->M;
+    HGM_TRY(zb.alloc(sizeof(int64_t) * (size_t)count * Mmax * MAX_BATCH_API, s));
+    // batches of consecutive models with equal chain length share one K-DP pass
+    const int max_batch = use_v0_kernels() ? 1 : MAX_BATCH_API;
+    for (int m0 = 0; m0 < n_models;) {
+        int m1 = m0 + 1;
+        while (m1 < n_models && m1 - m0 < max_batch && models[m1]->M == models[m0]->M) ++m1;
+        const int NM = m1 - m0, M = models[m0]->M;
+        HGM_TRY(mfeat.alloc(sizeof(float) * (size_t)NM * M * Fp, s));
+        for (int k = 0; k < NM; ++k)
+            HGM_CUDA(cudaMemcpyAsync(mfeat.as<float>() + (size_t)k * M * Fp, models[m0 + k]->feat,
+                                     sizeof(float) * (size_t)M * Fp, cudaMemcpyDeviceToDevice, s));
+        HGM_TRY(U.alloc(sizeof(float) * (size_t)NM * M * nn, s));
+        HGM_TRY(unary_table(mfeat.as<float>(), M, NM, Fp, scene, n_lo, n_hi, U.as<float>(), s));
+        MatchOut mo[MAX_BATCH_API];
+        for (int k = 0; k < NM; ++k)
+            mo[k] = MatchOut{Ed + (size_t)(m0 + k) * count, Ab.as<float>() + (size_t)(m0 + k) * count,
+                             zb.as<int64_t>() + (size_t)k * count * Mmax};
+        HGM_TRY(match_batch(models + m0, NM, scene, *params, *offsets, U.as<float>(), n_lo, nn, mo, s));
+        m0 = m1;
     }
+    scene->uses.record(s);
+    for (int m = 0; m < n_models; ++m) models[m]->uses.record(s);
     const bool hw = winner && !is_device_ptr(winner), hs = score && !is_device_ptr(score);
     if (hw) HGM_TRY(wdev.alloc(sizeof(int32_t) * count, s));
     if (hs) HGM_TRY(sdev.alloc(sizeof(float) * count, s));

@@ -17,43 +17,12 @@
 // candidate equal to the minimum -- exactly the first-strict-minimum rule (R11).
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
+#include <cstring>
 
-#include "hgm_device.cuh"
-#include "hgm_internal.cuh"
+#include "dp_common.cuh"
 
 namespace hgm {
-
-struct SceneView {
-    const int32_t *__restrict__ t;
-    const int32_t *__restrict__ ft;
-    const int32_t *__restrict__ qstart;
-    const float *__restrict__ theta;
-    const uint8_t *__restrict__ coinc;
-    const int32_t *__restrict__ prow;
-    const int64_t *__restrict__ id;
-    int fmax, S;
-    __device__ __forceinline__ int first(int f) const { return first_at(ft, fmax, S, f); }
-};
-
-struct InstDesc {
-    int32_t wb, we;   // window node range [wb, we)
-    int32_t pbase;    // band index of the window's first row = qstart[wb]
-    int32_t np;       // pair states of the window = qstart[we] - qstart[wb]
-    int64_t off;      // offset of this instance inside a layer
-    int32_t out;      // output slot (offset index)
-    int32_t pad;
-};
-
-struct StepConst {
-    float g_i, g_im1, A1, K2;  // model gaps (Eq. 5) and angle constants (Eq. 6), hgm_device.cuh
-};
-
-struct DPParams {
-    float l1, l2, l23, l1W, W;
-    int T;
-};
-
-__device__ __forceinline__ int ns_of(const InstDesc &d) { return d.np + 2 * (d.we - d.wb) + 1; }
 
 // ------------------------------------------------------------------ K-DP v0
 // One thread per state of one instance; candidates streamed from the band.
@@ -122,15 +91,6 @@ __global__ void __launch_bounds__(256) k_dp_step(SceneView sc, const InstDesc *_
 // ------------------------------------------------------------------ K-BT v0
 // One thread per instance: Eq. 13 init search, Eq. 12 backtrack by
 // re-evaluation, appearance distance.
-struct BTArgs {
-    const float *U;      // U rows of this model's nodes: U[i * nn + (n - n_lo)]
-    int64_t nn, n_lo;
-    const float4 *step;  // model step constants
-    int M;
-    float *E, *A;
-    int64_t *z;          // [count * M]
-};
-
 __global__ void k_backtrack(SceneView sc, const InstDesc *__restrict__ inst, int ninst, const float *__restrict__ hist,
                             int64_t L, BTArgs bt, DPParams p) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -181,7 +141,7 @@ __global__ void k_backtrack(SceneView sc, const InstDesc *__restrict__ inst, int
             }
         }
     }
-    int64_t *zo = bt.z ? bt.z + (int64_t)d.out * M : nullptr;
+    int64_t *zo = bt.z[0] ? bt.z[0] + (int64_t)d.out * M : nullptr;
     float A = z1b == EPS ? p.W : U(0, z1b);
     if (zo) zo[0] = z1b == EPS ? -1 : sc.id[z1b];
     if (M >= 2) {
@@ -192,7 +152,7 @@ __global__ void k_backtrack(SceneView sc, const InstDesc *__restrict__ inst, int
     int zb = z2b, za = z1b;
     for (int i = 2; i < M; ++i) {
         const float *nx = layer(i + 1);
-        const float4 kc = bt.step[i];
+        const float4 kc = bt.step[0][i];
         int zc = EPS;
         float R = INFINITY;
         if (zb != EPS && za != EPS) {
@@ -242,8 +202,8 @@ __global__ void k_backtrack(SceneView sc, const InstDesc *__restrict__ inst, int
         za = zb;
         zb = zc;
     }
-    if (bt.E) bt.E[d.out] = best;
-    if (bt.A) bt.A[d.out] = A;
+    if (bt.E[0]) bt.E[0][d.out] = best;
+    if (bt.A[0]) bt.A[0][d.out] = A;
 }
 
 // ------------------------------------------------------------------ K-ARG
@@ -274,87 +234,21 @@ hgm_status offset_argmin(const float *score, int n_models, int count, float thre
     HGM_CUDA(cudaGetLastError());
     return HGM_OK;
 }
-
-// ------------------------------------------------------------------ driver
-static inline int host_first(const hgm_scene *sc, int64_t f) {
-    if (f <= 0) return 0;
-    if (f > sc->fmax) return (int)sc->S;
-    return sc->first_h[f];
+// ------------------------------------------------------------------ v0 launchers
+// The v0 kernels (one thread per state / per instance, operands from global
+// memory) are kept as an independent second implementation of the same
+// arithmetic: tests require K-DP v0 and the batched K-DP to agree bit for bit.
+hgm_status launch_dp_v0(const SceneView &v, const InstDesc *dinst, int ninst, int64_t maxNs, float *hist, int64_t L,
+                        int layer, bool has_next, const StepConst &kc, const float *U, int64_t n_lo, const DPParams &p,
+                        cudaStream_t s) {
+    const dim3 grid((unsigned)((maxNs + 255) / 256), (unsigned)ninst);
+    k_dp_step<<<grid, 256, 0, s>>>(v, dinst, hist, L, layer, has_next, kc, U, n_lo, p);
+    return HGM_OK;
 }
 
-// Match one model at every offset: K-DP for steps M-1..2 (0-based), then K-BT.
-// U holds this model's rows: U[i * nn + (n - n_lo)].
-hgm_status match_model(const hgm_model *m, const hgm_scene *sc, const hgm_params &pp, const hgm_offsets &o,
-                       const float *U, int64_t n_lo, int64_t nn, MatchOut out, cudaStream_t s) {
-    const int count = o.count, M = m->M;
-    if (count <= 0) return HGM_OK;
-    std::vector<InstDesc> all(count);
-    for (int k = 0; k < count; ++k) {
-        const int64_t of = (int64_t)o.first_frame + (int64_t)k * o.stride;
-        InstDesc d{};
-        d.wb = host_first(sc, of);
-        d.we = host_first(sc, of + o.window);
-        d.pbase = sc->qstart_h[d.wb];
-        d.np = sc->qstart_h[d.we] - sc->qstart_h[d.wb];
-        d.out = k;
-        all[k] = d;
-    }
-    DPParams p;
-    p.l1 = pp.lambda1;
-    p.l2 = pp.lambda2;
-    p.l23 = pp.lambda2 * pp.lambda3;  // one IEEE single multiply
-    p.W = pp.w_dummy;
-    p.l1W = pp.lambda1 * pp.w_dummy;
-    p.T = pp.T;
-    const SceneView v{sc->t, sc->first_tab, sc->qstart, sc->theta, sc->coinc, sc->prow, sc->id, sc->fmax, (int)sc->S};
-    const int nsteps = M >= 3 ? M - 2 : 0;
-    const int64_t budget_floats = (int64_t)1 << 30;  // alpha history per chunk: 4 GiB
-    DevBuf hist, dinst;
-    int64_t hist_cap = 0;
-    HGM_TRY(dinst.alloc(sizeof(InstDesc) * std::min(count, 65535), s));
-    for (int k0 = 0; k0 < count;) {
-        int64_t L = 0;
-        int64_t maxNs = 1;
-        int k1 = k0;
-        while (k1 < count && k1 - k0 < 65535) {
-            InstDesc &d = all[k1];
-            const int64_t ns = (int64_t)d.np + 2 * (int64_t)(d.we - d.wb) + 1;
-            if (k1 > k0 && (L + ns) * std::max(nsteps, 1) > budget_floats) break;
-            d.off = L;
-            L += ns;
-            maxNs = std::max(maxNs, ns);
-            ++k1;
-        }
-        const int ninst = k1 - k0;
-        HGM_CUDA(cudaMemcpyAsync(dinst.p, all.data() + k0, sizeof(InstDesc) * ninst, cudaMemcpyHostToDevice, s));
-        const int64_t need = L * nsteps;
-        if (need > hist_cap) {
-            hist.release();
-            HGM_TRY(hist.alloc(sizeof(float) * need, s));
-            hist_cap = need;
-        }
-        if (nsteps > 0) {
-            Timer tm(s, K_DP);
-            const dim3 grid((unsigned)((maxNs + 255) / 256), (unsigned)ninst);
-            for (int i = M - 1; i >= 2; --i) {
-                const float4 h = m->step_h[i];
-                const StepConst kc{h.x, h.y, h.z, h.w};
-                k_dp_step<<<grid, 256, 0, s>>>(v, dinst.as<InstDesc>(), hist.as<float>(), L, i - 2, i + 1 <= M - 1,
-                                               kc, U + (int64_t)i * nn, n_lo, p);
-            }
-            count_launch(K_DP, nsteps);
-            HGM_CUDA(cudaGetLastError());
-        }
-        {
-            Timer tm(s, K_BT);
-            BTArgs bt{U, nn, n_lo, m->step, M, out.E, out.A, out.z};
-            k_backtrack<<<(ninst + 127) / 128, 128, 0, s>>>(v, dinst.as<InstDesc>(), ninst, hist.as<float>(), L, bt, p);
-            count_launch(K_BT);
-            HGM_CUDA(cudaGetLastError());
-        }
-        // dinst / hist are reused by the next chunk: stream order protects them
-        k0 = k1;
-    }
+hgm_status launch_backtrack_v0(const SceneView &v, const InstDesc *dinst, int ninst, const float *hist, int64_t L,
+                               const BTArgs &bt, const DPParams &p, cudaStream_t s) {
+    k_backtrack<<<(ninst + 127) / 128, 128, 0, s>>>(v, dinst, ninst, hist, L, bt, p);
     return HGM_OK;
 }
 

@@ -4,7 +4,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/hgm.h"
@@ -28,6 +30,8 @@ hgm_status cuda_fail(cudaError_t e, const char *what);
         if (s__ != HGM_OK) return s__;                                   \
     } while (0)
 
+constexpr int MAX_BATCH_API = 8;  // models of equal M matched together (dp_common.cuh MAX_BATCH)
+
 // Pad descriptors to a multiple of 4 floats so rows load as float4.
 inline int pad4(int F) { return (F + 3) & ~3; }
 
@@ -47,7 +51,19 @@ struct DevBuf {
 }  // namespace hgm
 
 // ------------------------------------------------------------------ handles
+// Handle arrays come from the stream-ordered pool.  Every call that reads a
+// handle records an event on its stream; hgm_free_* orders the frees after
+// those events on a private stream, so releasing a handle never blocks the
+// host or idles the GPU (a plain cudaFree synchronises the whole device).
+struct HandleUses {
+    std::mutex mu;
+    std::vector<std::pair<cudaStream_t, cudaEvent_t>> ev;
+    void record(cudaStream_t s);
+    void release_after(const std::vector<void *> &ptrs, int device);
+};
+
 struct hgm_scene {
+    mutable HandleUses uses;
     int device = 0;
     int64_t S = 0;     // number of scene nodes
     int F = 0, Fp = 0; // descriptor length, padded length
@@ -63,12 +79,21 @@ struct hgm_scene {
     int32_t *qstart = nullptr;  // [S + 1]: start of row a of the pair band
     float *theta = nullptr;     // [npairs]: direction of a -> c (K-G)
     uint8_t *coinc = nullptr;   // [npairs]: 1 if a and c coincide spatially (R10)
+    uint16_t *cpre = nullptr;   // [npairs]: inclusive prefix count of coinc along each row
+    // padded copy of the band for K-DP staging: row a starts at qpad[a] and has an odd
+    // padded length, so consecutive rows fall on distinct shared-memory banks when a
+    // tile's rows [A0, B1) are copied as ONE contiguous range
+    int32_t *qpad = nullptr;    // [S + 1]
+    float *theta_pad = nullptr; // [qpad[S]]
+    int32_t *rfc = nullptr;     // [S]: first coincident column of row a (INT_MAX if none)
+    int32_t *rlc = nullptr;     // [S]: last coincident column of row a (-1 if none)
     int32_t *prow = nullptr;    // [npairs]: the earlier node a of each pair
     // host mirrors (window / chunk sizing without device round-trips)
-    std::vector<int32_t> first_h, qstart_h;
+    std::vector<int32_t> first_h, qstart_h, qpad_h;
 };
 
 struct hgm_model {
+    mutable HandleUses uses;
     int device = 0;
     int M = 0, F = 0, Fp = 0;
     int32_t *t = nullptr;
@@ -82,7 +107,7 @@ struct hgm_model {
 namespace hgm {
 
 // ------------------------------------------------------------------ profiling
-enum KClass { K_SCENE = 0, K_MODEL = 1, K_UNARY = 2, K_DP = 3, K_BT = 4, K_ARG = 5 };
+enum KClass { K_SCENE = 0, K_MODEL = 1, K_UNARY = 2, K_DP = 3, K_BT = 4, K_ARG = 5, K_MSG = 6 };
 struct Timer {  // CUDA events on the launch stream, only when profiling is on
     cudaStream_t s;
     int cls;
@@ -97,17 +122,20 @@ bool profiling();
 hgm_status scene_build_device(const hgm_points *dev_pts, int32_t T_max, cudaStream_t s, hgm_scene **out);
 hgm_status model_build_device(const hgm_points *dev_pts, cudaStream_t s, hgm_model **out);
 
-// U[j][n - n_lo] = ||f_j - f'_n|| for j in [0, M_total), n in [n_lo, n_hi)
-hgm_status unary_table(const float *mfeat, int M_total, int Fp, const hgm_scene *sc, int64_t n_lo,
-                       int64_t n_hi, float *U, cudaStream_t s);
+// Unary table of a batch of NM models of M nodes each (model features stacked
+// model-major, node j = k*M + i), batched layout U[((i*nn) + (n - n_lo))*NM + k].
+hgm_status unary_table(const float *mfeat, int M, int NM, int Fp, const hgm_scene *sc, int64_t n_lo, int64_t n_hi,
+                       float *U, cudaStream_t s);
 
 struct MatchOut {  // per (model, offset) results of one model
     float *E;       // [count] device
     float *A;       // [count] device
     int64_t *z;     // [count * M] device
 };
-hgm_status match_model(const hgm_model *m, const hgm_scene *sc, const hgm_params &p, const hgm_offsets &o,
-                       const float *U, int64_t n_lo, int64_t nn, MatchOut out, cudaStream_t s);
+bool use_v0_kernels();
+hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *sc, const hgm_params &pp,
+                       const hgm_offsets &o, const float *U, int64_t n_lo, int64_t nn, const MatchOut *outs,
+                       cudaStream_t s);
 hgm_status offset_argmin(const float *score, int n_models, int count, float threshold, int32_t *winner,
                          float *best, cudaStream_t s);
 

@@ -64,22 +64,44 @@ __global__ void k_rowlen(int64_t S, int T_max, int fmax, const int32_t *__restri
     rowlen[a] = hi - lo;
 }
 
+__global__ void k_padlen(int64_t S, const int32_t *__restrict__ rowlen, int32_t *padlen) {
+    int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (a > S) return;
+    padlen[a] = a == S ? 0 : (rowlen[a] | 1);  // odd: consecutive rows on distinct banks
+}
+
 // K-G: direction band theta(a->c) and coincidence flags, one thread per row a
 __global__ void k_band(int64_t S, int T_max, int fmax, const int32_t *__restrict__ t, const float *__restrict__ x,
                        const float *__restrict__ y, const int32_t *__restrict__ ft, const int32_t *__restrict__ qstart,
-                       float *theta, uint8_t *coinc, int32_t *prow) {
+                       const int32_t *__restrict__ qpad, float *theta, float *theta_pad, uint8_t *coinc,
+                       uint16_t *cpre, int32_t *prow, int32_t *rfc, int32_t *rlc) {
     int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (a >= S) return;
     int lo = first_at(ft, fmax, (int)S, t[a] + 1);
     int hi = first_at(ft, fmax, (int)S, t[a] + T_max);
     float ax = x[a], ay = y[a];
     int64_t p = qstart[a];
+    float *tp = theta_pad + qpad[a];
+    unsigned run = 0;
+    int fc = 0x7fffffff, lc = -1;
     for (int c = lo; c < hi; ++c, ++p) {
         float cx = x[c], cy = y[c];
-        theta[p] = dir_of(ax, ay, cx, cy);
-        coinc[p] = (ax == cx && ay == cy) ? 1 : 0;
+        const bool co = ax == cx && ay == cy;
+        const float th = dir_of(ax, ay, cx, cy);
+        theta[p] = th;
+        tp[c - lo] = th;
+        coinc[p] = co ? 1 : 0;
+        run += co ? 1u : 0u;
+        cpre[p] = (uint16_t)min(run, 65535u);
         prow[p] = (int32_t)a;
+        if (co) {
+            fc = min(fc, c - lo);
+            lc = c - lo;
+        }
     }
+    if (((hi - lo) & 1) == 0) tp[hi - lo] = 0.f;  // padding slot
+    rfc[a] = fc;
+    rlc[a] = lc;
 }
 
 static hgm_status sort_by_frame(const int32_t *frame, int64_t n, int32_t *keys_out, int32_t *order,
@@ -99,7 +121,9 @@ static hgm_status sort_by_frame(const int32_t *frame, int64_t n, int32_t *keys_o
 }
 
 static void free_scene_dev(hgm_scene *sc) {
-    void *ptrs[] = {sc->t, sc->x, sc->y, sc->feat, sc->id, sc->first_tab, sc->qstart, sc->theta, sc->coinc, sc->prow};
+    void *ptrs[] = {sc->t,      sc->x,     sc->y,     sc->feat, sc->id,  sc->first_tab,
+                    sc->qstart, sc->theta, sc->coinc, sc->cpre, sc->prow,
+                    sc->qpad,   sc->theta_pad, sc->rfc, sc->rlc};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -114,6 +138,7 @@ hgm_status scene_build_device(const hgm_points *pts, int32_t T_max, cudaStream_t
     sc->F = pts->F;
     sc->Fp = pad4(pts->F);
     sc->T_max = T_max;
+    auto dmalloc = [&](auto **ptr, size_t bytes) { return cudaMallocAsync((void **)ptr, bytes, s); };
     auto bail = [&](hgm_status st) {
         free_scene_dev(sc);
         delete sc;
@@ -124,12 +149,12 @@ hgm_status scene_build_device(const hgm_points *pts, int32_t T_max, cudaStream_t
         cudaError_t e__ = (call);                                        \
         if (e__ != cudaSuccess) return bail(cuda_fail(e__, #call));      \
     } while (0)
-    SC_CUDA(cudaMalloc(&sc->t, sizeof(int32_t) * n));
-    SC_CUDA(cudaMalloc(&sc->x, sizeof(float) * n));
-    SC_CUDA(cudaMalloc(&sc->y, sizeof(float) * n));
-    SC_CUDA(cudaMalloc(&sc->feat, sizeof(float) * n * sc->Fp));
-    SC_CUDA(cudaMalloc(&sc->id, sizeof(int64_t) * n));
-    SC_CUDA(cudaMalloc(&sc->qstart, sizeof(int32_t) * (n + 1)));
+    SC_CUDA(dmalloc(&sc->t, sizeof(int32_t) * n));
+    SC_CUDA(dmalloc(&sc->x, sizeof(float) * n));
+    SC_CUDA(dmalloc(&sc->y, sizeof(float) * n));
+    SC_CUDA(dmalloc(&sc->feat, sizeof(float) * n * sc->Fp));
+    SC_CUDA(dmalloc(&sc->id, sizeof(int64_t) * n));
+    SC_CUDA(dmalloc(&sc->qstart, sizeof(int32_t) * (n + 1)));
     {
         DevBuf order;
         if (order.alloc(sizeof(int32_t) * n, s) != HGM_OK) return bail(HGM_ERR_OUT_OF_MEMORY);
@@ -147,7 +172,7 @@ hgm_status scene_build_device(const hgm_points *pts, int32_t T_max, cudaStream_t
     SC_CUDA(cudaStreamSynchronize(s));
     if (tt[0] < 0) return bail(fail(HGM_ERR_INVALID_ARGUMENT, "negative frame index"));
     sc->fmax = tt[1];
-    SC_CUDA(cudaMalloc(&sc->first_tab, sizeof(int32_t) * (sc->fmax + 2)));
+    SC_CUDA(dmalloc(&sc->first_tab, sizeof(int32_t) * (sc->fmax + 2)));
     k_first_tab<<<(unsigned)((n + 1 + 255) / 256), 256, 0, s>>>(n, sc->t, sc->first_tab);
     DevBuf rowlen, tmp;
     if (rowlen.alloc(sizeof(int32_t) * (n + 1), s) != HGM_OK) return bail(HGM_ERR_OUT_OF_MEMORY);
@@ -158,23 +183,39 @@ hgm_status scene_build_device(const hgm_points *pts, int32_t T_max, cudaStream_t
     SC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, rowlen.as<int32_t>(), sc->qstart, (int)(n + 1), s));
     if (tmp.alloc(tb, s) != HGM_OK) return bail(HGM_ERR_OUT_OF_MEMORY);
     SC_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, rowlen.as<int32_t>(), sc->qstart, (int)(n + 1), s));
-    count_launch(K_SCENE);
+    // padded band offsets (odd row lengths)
+    SC_CUDA(dmalloc(&sc->qpad, sizeof(int32_t) * (n + 1)));
+    {
+        DevBuf padlen;
+        if (padlen.alloc(sizeof(int32_t) * (n + 1), s) != HGM_OK) return bail(HGM_ERR_OUT_OF_MEMORY);
+        k_padlen<<<(unsigned)((n + 1 + 255) / 256), 256, 0, s>>>(n, rowlen.as<int32_t>(), padlen.as<int32_t>());
+        SC_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, padlen.as<int32_t>(), sc->qpad, (int)(n + 1), s));
+    }
+    count_launch(K_SCENE, 3);
     sc->first_h.resize(sc->fmax + 2);
     sc->qstart_h.resize(n + 1);
+    sc->qpad_h.resize(n + 1);
     SC_CUDA(cudaMemcpyAsync(sc->first_h.data(), sc->first_tab, sizeof(int32_t) * (sc->fmax + 2),
                             cudaMemcpyDeviceToHost, s));
     SC_CUDA(cudaMemcpyAsync(sc->qstart_h.data(), sc->qstart, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, s));
+    SC_CUDA(cudaMemcpyAsync(sc->qpad_h.data(), sc->qpad, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, s));
     SC_CUDA(cudaStreamSynchronize(s));
     sc->npairs = sc->qstart_h[n];
+    if (sc->qpad_h[n] < sc->npairs) return bail(fail(HGM_ERR_INVALID_ARGUMENT, "pair band exceeds 2^31 entries"));
+    SC_CUDA(dmalloc(&sc->rfc, sizeof(int32_t) * n));
+    SC_CUDA(dmalloc(&sc->rlc, sizeof(int32_t) * n));
+    SC_CUDA(dmalloc(&sc->theta_pad, sizeof(float) * ((int64_t)sc->qpad_h[n] + 4)));
     if (sc->npairs > 0) {
-        SC_CUDA(cudaMalloc(&sc->theta, sizeof(float) * sc->npairs));
-        SC_CUDA(cudaMalloc(&sc->coinc, sizeof(uint8_t) * sc->npairs));
-        SC_CUDA(cudaMalloc(&sc->prow, sizeof(int32_t) * sc->npairs));
-        k_band<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(n, T_max, sc->fmax, sc->t, sc->x, sc->y, sc->first_tab,
-                                                           sc->qstart, sc->theta, sc->coinc, sc->prow);
-        count_launch(K_SCENE);
-        SC_CUDA(cudaGetLastError());
+        SC_CUDA(dmalloc(&sc->theta, sizeof(float) * sc->npairs));
+        SC_CUDA(dmalloc(&sc->coinc, sizeof(uint8_t) * sc->npairs));
+        SC_CUDA(dmalloc(&sc->cpre, sizeof(uint16_t) * sc->npairs));
+        SC_CUDA(dmalloc(&sc->prow, sizeof(int32_t) * sc->npairs));
     }
+    k_band<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(n, T_max, sc->fmax, sc->t, sc->x, sc->y, sc->first_tab,
+                                                       sc->qstart, sc->qpad, sc->theta, sc->theta_pad, sc->coinc,
+                                                       sc->cpre, sc->prow, sc->rfc, sc->rlc);
+    count_launch(K_SCENE);
+    SC_CUDA(cudaGetLastError());
     SC_CUDA(cudaStreamSynchronize(s));
 #undef SC_CUDA
     *out = sc;
@@ -264,12 +305,13 @@ hgm_status model_build_device(const hgm_points *pts, cudaStream_t s, hgm_model *
     m->M = M;
     m->F = pts->F;
     m->Fp = pad4(pts->F);
+    auto dmalloc = [&](auto **ptr, size_t bytes) { return cudaMallocAsync((void **)ptr, bytes, s); };
     cudaError_t e = cudaSuccess;
-    if (e == cudaSuccess) e = cudaMalloc(&m->t, sizeof(int32_t) * M);
-    if (e == cudaSuccess) e = cudaMalloc(&m->x, sizeof(float) * M);
-    if (e == cudaSuccess) e = cudaMalloc(&m->y, sizeof(float) * M);
-    if (e == cudaSuccess) e = cudaMalloc(&m->feat, sizeof(float) * M * m->Fp);
-    if (e == cudaSuccess) e = cudaMalloc(&m->step, sizeof(float4) * M);
+    if (e == cudaSuccess) e = dmalloc(&m->t, sizeof(int32_t) * M);
+    if (e == cudaSuccess) e = dmalloc(&m->x, sizeof(float) * M);
+    if (e == cudaSuccess) e = dmalloc(&m->y, sizeof(float) * M);
+    if (e == cudaSuccess) e = dmalloc(&m->feat, sizeof(float) * M * m->Fp);
+    if (e == cudaSuccess) e = dmalloc(&m->step, sizeof(float4) * M);
     if (e != cudaSuccess) {
         hgm_free_model(m);
         return cuda_fail(e, "cudaMalloc(model)");

@@ -20,9 +20,10 @@ namespace hgm {
 constexpr int KU_TN = 128;  // scene nodes per CTA (one per thread)
 constexpr int KU_TJ = 8;    // model nodes per register tile
 
-__global__ void __launch_bounds__(KU_TN) k_unary(const float *__restrict__ mfeat, int M_total, int Fp,
+__global__ void __launch_bounds__(KU_TN) k_unary(const float *__restrict__ mfeat, int M, int NM, int Fp,
                                                  const float *__restrict__ sfeat, int64_t n_lo, int64_t nn,
                                                  float *__restrict__ U) {
+    const int M_total = M * NM;
     extern __shared__ float4 sm[];  // [KU_TJ][Fp/4] model descriptors
     const int F4 = Fp >> 2;
     const int64_t n = blockIdx.x * (int64_t)KU_TN + threadIdx.x;
@@ -55,21 +56,23 @@ __global__ void __launch_bounds__(KU_TN) k_unary(const float *__restrict__ mfeat
         if (live) {
 #pragma unroll
             for (int q = 0; q < KU_TJ; ++q)
-                if (q < nj)
-                    U[(int64_t)(j0 + q) * nn + n] =
+                if (q < nj) {
+                    const int j = j0 + q, k = j / M, i = j - k * M;  // node j = k*M + i of model k
+                    U[((int64_t)i * nn + n) * NM + k] =
                         __fsqrt_rn(__fadd_rn(__fadd_rn(acc[q][0], acc[q][1]), __fadd_rn(acc[q][2], acc[q][3])));
+                }
         }
     }
 }
 
-hgm_status unary_table(const float *mfeat, int M_total, int Fp, const hgm_scene *sc, int64_t n_lo, int64_t n_hi,
+hgm_status unary_table(const float *mfeat, int M, int NM, int Fp, const hgm_scene *sc, int64_t n_lo, int64_t n_hi,
                        float *U, cudaStream_t s) {
     const int64_t nn = n_hi - n_lo;
-    if (nn <= 0 || M_total <= 0) return HGM_OK;
+    if (nn <= 0 || M * NM <= 0) return HGM_OK;
     Timer tm(s, K_UNARY);
     const size_t smem = sizeof(float) * KU_TJ * Fp;
     if (smem > 48 * 1024) HGM_CUDA(cudaFuncSetAttribute(k_unary, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_unary<<<(unsigned)((nn + KU_TN - 1) / KU_TN), KU_TN, smem, s>>>(mfeat, M_total, Fp, sc->feat, n_lo, nn, U);
+    k_unary<<<(unsigned)((nn + KU_TN - 1) / KU_TN), KU_TN, smem, s>>>(mfeat, M, NM, Fp, sc->feat, n_lo, nn, U);
     count_launch(K_UNARY);
     HGM_CUDA(cudaGetLastError());
     return HGM_OK;

@@ -52,7 +52,7 @@ class Offsets(C.Structure):
 
 
 class Stats(C.Structure):
-    _fields_ = [("ms", C.c_double * 6), ("launches", C.c_int64 * 6), ("dp_candidates", C.c_int64),
+    _fields_ = [("ms", C.c_double * 8), ("launches", C.c_int64 * 8), ("dp_candidates", C.c_int64),
                 ("dp_states", C.c_int64), ("dp_launches", C.c_int64)]
 
 
@@ -293,7 +293,7 @@ def set_profiling(enable: bool = True):
 def get_stats(reset: bool = False) -> dict:
     s = Stats()
     _check(lib().hgm_get_stats(C.byref(s), int(bool(reset))))
-    names = ("scene", "model", "unary", "dp", "backtrack", "argmin")
+    names = ("scene", "model", "unary", "dp", "backtrack", "argmin", "msg", "reserved")
     return dict(ms={n: s.ms[i] for i, n in enumerate(names)},
                 launches={n: s.launches[i] for i, n in enumerate(names)}, dp_launches=s.dp_launches)
 

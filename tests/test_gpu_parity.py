@@ -198,6 +198,68 @@ def test_device_builders_match_host_builders(hgm):
     assert torch.equal(a.E, b.E) and torch.equal(a.z, b.z)
 
 
+@pytest.mark.parametrize("name,kw", [("C1", {}), ("C2", {}), ("C3", dict(n_frames=1500)), ("C0", dict(seed=3))])
+def test_tiled_kernel_bitexact_to_reference_kernel(hgm, name, kw, monkeypatch):
+    """K-DP v1 (tiled, shared memory) and K-DP v0 (one thread per state) run the
+    same per-candidate arithmetic (hgm_device.cuh): results must be bit-identical."""
+    import torch
+
+    wl = synth.make_workload(name, **kw)
+    p = wl.params()
+    s = hgm.build_scene_index(wl.scenes[0], device=0, T_max=p["T"])
+    out = {}
+    for kern in ("v0", "v1"):
+        monkeypatch.setenv("HGM_KERNEL", kern)
+        res = []
+        for mp in wl.models:
+            m = hgm.build_model_graph(mp, device=0)
+            res.append(hgm.match_model_at_offsets(m, s, p, wl.first[0], wl.stride, wl.count[0], wl.window))
+        torch.cuda.synchronize()
+        out[kern] = res
+    for a, b in zip(out["v0"], out["v1"]):
+        assert torch.equal(a.E, b.E) and torch.equal(a.A, b.A) and torch.equal(a.z, b.z)
+
+
+@pytest.mark.parametrize("name,kw", [("C2", {}), ("C3", dict(n_frames=2000)), ("C4", dict(T=10, n_frames=900))])
+def test_model_batched_kernel_bitexact(hgm, name, kw, monkeypatch):
+    """detect_actions batches the 6 models of equal M into one K-DP pass; the
+    per-model reference kernels (HGM_KERNEL=v0) must give identical bits."""
+    import torch
+
+    wl = synth.make_workload(name, **kw)
+    p = wl.params()
+    s = hgm.build_scene_index(wl.scenes[0], device=0, T_max=p["T"])
+    models = [hgm.build_model_graph(m, device=0) for m in wl.models]
+    res = {}
+    for kern in ("v0", "v1"):
+        monkeypatch.setenv("HGM_KERNEL", kern)
+        for mode in (0, 1):
+            r = hgm.detect_actions(models, s, p, wl.first[0], wl.stride, wl.count[0], wl.window, score_mode=mode,
+                                   want_E_all=True)
+            torch.cuda.synchronize()
+            res[(kern, mode)] = r
+    for mode in (0, 1):
+        a, b = res[("v0", mode)], res[("v1", mode)]
+        assert torch.equal(a.E_all, b.E_all) and torch.equal(a.winner, b.winner) and torch.equal(a.score, b.score)
+
+
+@pytest.mark.parametrize("ft", [1, 3, 8])
+def test_tile_sizes_bitexact(hgm, ft, monkeypatch):
+    import torch
+
+    wl = synth.make_workload("C1")
+    p = wl.params()
+    s = hgm.build_scene_index(wl.scenes[0], device=0, T_max=10)
+    m = hgm.build_model_graph(wl.models[0], device=0)
+    monkeypatch.setenv("HGM_KERNEL", "v0")
+    a = hgm.match_model_at_offsets(m, s, p, 0, 1, 541, 60)
+    monkeypatch.setenv("HGM_KERNEL", "v1")
+    monkeypatch.setenv("HGM_TILE_FRAMES", str(ft))
+    b = hgm.match_model_at_offsets(m, s, p, 0, 1, 541, 60)
+    torch.cuda.synchronize()
+    assert torch.equal(a.E, b.E) and torch.equal(a.z, b.z)
+
+
 def test_bit_determinism(hgm):
     import torch
 
