@@ -298,7 +298,7 @@ hgm_status hgm_scene_num_nodes(const hgm_scene *sc, int64_t *S) {
 void hgm_free_scene(hgm_scene *sc) {
     if (!sc) return;
     sc->uses.release_after({sc->t, sc->x, sc->y, sc->feat, sc->id, sc->first_tab, sc->qstart, sc->theta, sc->coinc,
-                            sc->cpre, sc->prow, sc->qpad, sc->theta_pad, sc->rfc, sc->rlc},
+                            sc->cpre, sc->prow, sc->qpad, sc->theta_pad, sc->rfc, sc->rlc, sc->ninfo},
                            sc->device);
     delete sc;
 }

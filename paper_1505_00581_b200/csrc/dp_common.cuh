@@ -17,6 +17,7 @@ struct SceneView {
     const int32_t *__restrict__ qpad;      // padded band (K-DP staging)
     const float *__restrict__ theta_pad;
     const int32_t *__restrict__ rfc, *__restrict__ rlc;  // per-row first / last coincident column
+    const int4 *__restrict__ ninfo;  // (t', minnode(t'+1), qstart, qpad) per node
     int fmax, S;
     __device__ __forceinline__ int first(int f) const { return first_at(ft, fmax, S, f); }
     // coincident pairs in row x, columns [j0, j1)

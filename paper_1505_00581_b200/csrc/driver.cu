@@ -11,11 +11,11 @@
 namespace hgm {
 
 hgm_status launch_dp_batch(int NM, const SceneView &v, const InstDesc *dinst, int ninst, float *hist, int64_t L,
-                           int layer, bool has_next, const StepConstB &kc, const float *Ui, const float *Uprev,
-                           const float *msg_in, float *msg_out, const DPParams &p, const TileGeom &tg,
-                           cudaStream_t s);
-hgm_status launch_msg0(int NM, const SceneView &v, const InstDesc *dinst, int ninst, int max_sw, int T,
-                       const float *Ui, float *msg, float l1, cudaStream_t s);
+                           int layer, bool has_next, bool has_prev, const StepConstB &kc, const float *msg,
+                           const DPParams &p, const TileGeom &tg, cudaStream_t s);
+hgm_status launch_msg(int NM, const SceneView &v, const InstDesc *dinst, int ninst, int max_np, int max_sw,
+                      float *hist, int64_t L, int layer, bool has_next, bool init, const StepConstB &kc,
+                      const float *Ui, float *msg, const DPParams &p, int W, cudaStream_t s);
 size_t dp_batch_smem(const TileGeom &tg, int T, int NM);
 hgm_status launch_backtrack_warp(const SceneView &v, const InstDesc *dinst, int ninst, const float *hist, int64_t L,
                                  const BTArgs &bt, const DPParams &p, cudaStream_t s);
@@ -127,7 +127,7 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
     p.T = pp.T;
     const SceneView v{sc->t,    sc->first_tab, sc->qstart, sc->theta,     sc->coinc, sc->cpre,
                       sc->prow, sc->id,        sc->qpad,   sc->theta_pad, sc->rfc,   sc->rlc,
-                      sc->fmax, (int)sc->S};
+                      sc->ninfo, sc->fmax,     (int)sc->S};
     const int nsteps = M >= 3 ? M - 2 : 0;
     // Windows are processed in chunks (the alpha history of a chunk must fit the
     // budget).  Chunks alternate between two streams, so the streaming K-MSG of
@@ -170,7 +170,7 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
         Lane &ln = lanes[chunk % nlanes];
         const cudaStream_t ls = ln.s;
         int64_t L = 0, maxNs = 1, MS = 0;
-        int k1 = k0, max_sw = 1;
+        int k1 = k0, max_sw = 1, max_np = 1;
         while (k1 < count && k1 - k0 < chunk_max) {
             InstDesc &d = all[k1];
             const int64_t ns = (int64_t)d.np + 2 * (int64_t)(d.we - d.wb) + 1;
@@ -182,6 +182,7 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
             MS += (((int64_t)sc->qpad_h[d.we] - d.ppad) * NMP + 3) & ~(int64_t)3;  // 16-byte aligned rows
             maxNs = std::max(maxNs, ns);
             max_sw = std::max(max_sw, d.we - d.wb);
+            max_np = std::max(max_np, d.np);
             ++k1;
         }
         const int ninst = k1 - k0;
@@ -200,34 +201,38 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
             if ((st = ln.hist.alloc(sizeof(float) * need, ls)) != HGM_OK) break;
             ln.hist_cap = need;
         }
-        if (!v0 && nsteps > 0 && 2 * (MS + 4) > ln.msg_cap) {  // double-buffered partial messages
-            if ((st = ln.msg.alloc(sizeof(float) * 2 * (MS + 4), ls)) != HGM_OK) break;
-            ln.msg_cap = 2 * (MS + 4);
+        if (!v0 && nsteps > 0 && MS + 4 > ln.msg_cap) {
+            if ((st = ln.msg.alloc(sizeof(float) * (MS + 4), ls)) != HGM_OK) break;
+            ln.msg_cap = MS + 4;
         }
         const InstDesc *di = ln.dinst.as<InstDesc>();
         float *hist = ln.hist.as<float>();
         auto Urow = [&](int i) { return U + ((int64_t)i * nn - n_lo) * NM; };  // batched row, Urow(i)[c*NM + k]
-        auto mbuf = [&](int i) { return ln.msg.as<float>() + (int64_t)(i & 1) * (MS + 4); };
-        if (!v0 && nsteps > 0) {  // partial messages of the first step (alpha_{M+1} = 0)
-            Timer tm(ls, K_MSG);
-            st = launch_msg0(NM, v, di, ninst, max_sw, pp.T, Urow(M - 1), mbuf(M - 1), p.l1, ls);
-            count_launch(K_MSG);
-        }
         for (int i = M - 1; i >= 2 && st == HGM_OK; --i) {
             const bool has_next = i + 1 <= M - 1;
-            Timer tm(ls, K_DP);
             if (v0) {
+                Timer tm(ls, K_DP);
                 const float4 h = models[0]->step_h[i];
                 const StepConst kc{h.x, h.y, h.z, h.w};
                 st = launch_dp_v0(v, di, ninst, maxNs, hist, L, i - 2, has_next, kc, U + (int64_t)i * nn, n_lo, p, ls);
-            } else {
-                StepConstB kc{};
-                for (int k = 0; k < NM; ++k) kc.c[k] = models[k]->step_h[i];
-                const bool emit = i - 1 >= 2;  // the epilogue writes the next step's partial messages
-                st = launch_dp_batch(NM, v, di, ninst, hist, L, i - 2, has_next, kc, Urow(i),
-                                     emit ? Urow(i - 1) : nullptr, mbuf(i), emit ? mbuf(i - 1) : nullptr, p, tg, ls);
+                count_launch(K_DP);
+                continue;
             }
-            count_launch(K_DP);
+            StepConstB kc{};
+            for (int k = 0; k < NM; ++k) kc.c[k] = models[k]->step_h[i];
+            {
+                Timer tm(ls, K_MSG);
+                st = launch_msg(NM, v, di, ninst, max_np, max_sw, hist, L, i - 2, has_next, /*init=*/!has_next, kc,
+                                Urow(i), ln.msg.as<float>(), p, o.window, ls);
+                count_launch(K_MSG, has_next ? 1 : 2);
+            }
+            if (st != HGM_OK) break;
+            {
+                Timer tm(ls, K_DP);
+                st = launch_dp_batch(NM, v, di, ninst, hist, L, i - 2, has_next, /*has_prev=*/i - 1 >= 2, kc,
+                                     ln.msg.as<float>(), p, tg, ls);
+                count_launch(K_DP);
+            }
         }
         if (st != HGM_OK) break;
         if ((e = cudaGetLastError()) != cudaSuccess) {

@@ -87,6 +87,7 @@ struct hgm_scene {
     float *theta_pad = nullptr; // [qpad[S]]
     int32_t *rfc = nullptr;     // [S]: first coincident column of row a (INT_MAX if none)
     int32_t *rlc = nullptr;     // [S]: last coincident column of row a (-1 if none)
+    int4 *ninfo = nullptr;      // [S]: (t'(x), minnode(t'(x)+1), qstart[x], qpad[x]) -- one load per row
     int32_t *prow = nullptr;    // [npairs]: the earlier node a of each pair
     // host mirrors (window / chunk sizing without device round-trips)
     std::vector<int32_t> first_h, qstart_h, qpad_h;

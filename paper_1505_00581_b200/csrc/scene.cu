@@ -104,6 +104,13 @@ __global__ void k_band(int64_t S, int T_max, int fmax, const int32_t *__restrict
     rlc[a] = lc;
 }
 
+__global__ void k_ninfo(int64_t S, int fmax, const int32_t *__restrict__ t, const int32_t *__restrict__ ft,
+                        const int32_t *__restrict__ qstart, const int32_t *__restrict__ qpad, int4 *ninfo) {
+    int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (a >= S) return;
+    ninfo[a] = make_int4(t[a], first_at(ft, fmax, (int)S, t[a] + 1), qstart[a], qpad[a]);
+}
+
 static hgm_status sort_by_frame(const int32_t *frame, int64_t n, int32_t *keys_out, int32_t *order,
                                 cudaStream_t s) {
     DevBuf iota, tmp;
@@ -123,7 +130,7 @@ static hgm_status sort_by_frame(const int32_t *frame, int64_t n, int32_t *keys_o
 static void free_scene_dev(hgm_scene *sc) {
     void *ptrs[] = {sc->t,      sc->x,     sc->y,     sc->feat, sc->id,  sc->first_tab,
                     sc->qstart, sc->theta, sc->coinc, sc->cpre, sc->prow,
-                    sc->qpad,   sc->theta_pad, sc->rfc, sc->rlc};
+                    sc->qpad,   sc->theta_pad, sc->rfc, sc->rlc, sc->ninfo};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -214,7 +221,10 @@ hgm_status scene_build_device(const hgm_points *pts, int32_t T_max, cudaStream_t
     k_band<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(n, T_max, sc->fmax, sc->t, sc->x, sc->y, sc->first_tab,
                                                        sc->qstart, sc->qpad, sc->theta, sc->theta_pad, sc->coinc,
                                                        sc->cpre, sc->prow, sc->rfc, sc->rlc);
-    count_launch(K_SCENE);
+    SC_CUDA(dmalloc(&sc->ninfo, sizeof(int4) * n));
+    k_ninfo<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, sc->fmax, sc->t, sc->first_tab, sc->qstart, sc->qpad,
+                                                        sc->ninfo);
+    count_launch(K_SCENE, 2);
     SC_CUDA(cudaGetLastError());
     SC_CUDA(cudaStreamSynchronize(s));
 #undef SC_CUDA

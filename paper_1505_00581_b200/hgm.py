@@ -15,7 +15,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libhgm.so")
+LIB_PATH = os.environ.get("HGM_LIB") or os.path.join(_HERE, "lib", "libhgm.so")  # HGM_LIB: A/B builds
 
 STATUS = {0: "HGM_OK", 1: "HGM_ERR_EMPTY_POINT_SET", 2: "HGM_ERR_DIMENSION_MISMATCH",
           3: "HGM_ERR_INVALID_ARGUMENT", 4: "HGM_ERR_OUT_OF_MEMORY", 5: "HGM_ERR_CUDA"}
