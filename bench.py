@@ -277,8 +277,15 @@ def main():
     f_mhz = ck["sm_mhz"] or 1965.0
     achieved = work_cand / (dp_ms / 1000.0) / 1e9  # G real-triple candidates / s
     peak = LANES_PER_CLK * f_mhz * 1e6 / ISSUE_SLOTS_PER_CAND / 1e9
-    roof = dict(bound="alu", achieved=achieved, peak=peak, unit="Gcand/s", frac=achieved / peak, traffic=None,
-                kernel="k_dp_step", dp_ms_per_step=dp_ms, dp_share_of_step=dp_ms / ms_step,
+    traffic, traffic_src = None, None
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "dp_traffic.json")
+    if os.path.exists(tpath):  # DRAM bytes per K-DP launch from the committed ncu --set full capture
+        with open(tpath) as fh:
+            tj = json.load(fh)
+        traffic, traffic_src = tj.get("dram_bytes_per_launch"), tj.get("source")
+    roof = dict(bound="alu", achieved=achieved, peak=peak, unit="Gcand/s", frac=achieved / peak, traffic=traffic,
+                traffic_unit="DRAM bytes per K-DP launch", traffic_source=traffic_src,
+                kernel="k_dp_batch", dp_ms_per_step=dp_ms, dp_share_of_step=dp_ms / ms_step,
                 candidates_per_step=work_cand, states_per_step=work_states,
                 peak_basis=f"148 SMs x 128 lanes x {f_mhz:.0f} MHz (median SM clock sampled in the timed region)"
                            f" / {ISSUE_SLOTS_PER_CAND} issue slots per real-triple candidate",
