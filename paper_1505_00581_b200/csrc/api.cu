@@ -298,7 +298,8 @@ hgm_status hgm_scene_num_nodes(const hgm_scene *sc, int64_t *S) {
 void hgm_free_scene(hgm_scene *sc) {
     if (!sc) return;
     sc->uses.release_after({sc->t, sc->x, sc->y, sc->feat, sc->id, sc->first_tab, sc->qstart, sc->theta, sc->coinc,
-                            sc->cpre, sc->prow, sc->qpad, sc->theta_pad, sc->rfc, sc->rlc, sc->ninfo},
+                            sc->cpre, sc->prow, sc->qpad, sc->theta_pad, sc->prow_pad, sc->rfc, sc->rlc,
+                            sc->ninfo},
                            sc->device);
     delete sc;
 }
@@ -325,7 +326,7 @@ hgm_status hgm_match_model_at_offsets(const hgm_model *model, const hgm_scene *s
     covered_range(scene, offsets, &n_lo, &n_hi);
     const int64_t nn = std::max<int64_t>(n_hi - n_lo, 1);
     DevBuf U, dE, dA, dz;
-    HGM_TRY(U.alloc(sizeof(float) * (size_t)model->M * nn, s));
+    HGM_TRY(U.alloc(sizeof(float) * ((size_t)model->M * nn + 4), s));  // + 16 B: K-DP bulk-copy rounding
     HGM_TRY(unary_table(model->feat, model->M, 1, model->Fp, scene, n_lo, n_hi, U.as<float>(), s));
     const bool hE = E && !is_device_ptr(E), hA = A && !is_device_ptr(A), hz = z && !is_device_ptr(z);
     if (hE) HGM_TRY(dE.alloc(sizeof(float) * count, s));
@@ -385,7 +386,7 @@ hgm_status hgm_detect_actions(const hgm_model *const *models, int32_t n_models, 
         for (int k = 0; k < NM; ++k)
             HGM_CUDA(cudaMemcpyAsync(mfeat.as<float>() + (size_t)k * M * Fp, models[m0 + k]->feat,
                                      sizeof(float) * (size_t)M * Fp, cudaMemcpyDeviceToDevice, s));
-        HGM_TRY(U.alloc(sizeof(float) * (size_t)NM * M * nn, s));
+        HGM_TRY(U.alloc(sizeof(float) * ((size_t)NM * M * nn + 4), s));  // + 16 B: K-DP bulk-copy rounding
         HGM_TRY(unary_table(mfeat.as<float>(), M, NM, Fp, scene, n_lo, n_hi, U.as<float>(), s));
         MatchOut mo[MAX_BATCH_API];
         for (int k = 0; k < NM; ++k)

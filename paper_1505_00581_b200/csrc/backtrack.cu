@@ -38,9 +38,10 @@ __global__ void __launch_bounds__(128) k_backtrack_warp(SceneView sc, const Inst
         return (i >= 2 && i <= M - 1) ? hist + (int64_t)(i - 2) * L + d.off : nullptr;
     };
     auto at = [&](const float *l, int s) { return l ? l[(int64_t)s * NM + kk] : 0.f; };
-    auto a_be = [&](const float *l, int b) { return at(l, d.np + (b - d.wb)); };
-    auto a_ea = [&](const float *l, int a) { return at(l, d.np + Sw + (a - d.wb)); };
-    auto a_ee = [&](const float *l) { return at(l, d.np + 2 * Sw); };
+    // layer layout (dp_common.cuh): pair state (later, earlier) at qpad[earlier] - ppad + column
+    auto a_be = [&](const float *l, int b) { return at(l, d.ntail + (b - d.wb)); };
+    auto a_ea = [&](const float *l, int a) { return at(l, d.ntail + Sw + (a - d.wb)); };
+    auto a_ee = [&](const float *l) { return at(l, d.ntail + 2 * Sw); };
 
     // ---- Eq. 13 init search
     Best best{INFINITY, 0x7fffffff, 0x7fffffff};
@@ -59,13 +60,13 @@ __global__ void __launch_bounds__(128) k_backtrack_warp(SceneView sc, const Inst
                 lo = sc.first(sc.t[z1] + 1);
                 c0 = lo;
                 c1 = min(sc.first(sc.t[z1] + T), d.we);
-                q = sc.qstart[z1];
+                q = sc.qpad[z1];
             }
             for (int z2 = c0; z2 <= c1; ++z2) {
                 const bool r2 = z2 < c1;
                 const float u2 = r2 ? __fmul_rn(p.l1, U(1, z2)) : p.l1W;
                 float al;
-                if (r1 && r2) al = at(a3, q + (z2 - lo) - d.pbase);
+                if (r1 && r2) al = at(a3, q + (z2 - lo) - d.ppad);
                 else if (r1) al = a_ea(a3, z1);
                 else if (r2) al = a_be(a3, z2);
                 else al = a_ee(a3);
@@ -106,7 +107,7 @@ __global__ void __launch_bounds__(128) k_backtrack_warp(SceneView sc, const Inst
         }
         float th_ab = 0.f;
         bool co_ab = false;
-        int qa = 0, qb = 0, aoff = 0, tb = 0;
+        int qa = 0, qb = 0, qbp = 0, aoff = 0, tb = 0;
         if (rb && ra) {
             qa = sc.qstart[za];
             const int loa = sc.first(sc.t[za] + 1);
@@ -116,12 +117,13 @@ __global__ void __launch_bounds__(128) k_backtrack_warp(SceneView sc, const Inst
         }
         if (rb) {
             qb = sc.qstart[zb];
+            qbp = sc.qpad[zb] - d.ppad;
             tb = sc.t[zb];
         }
         auto value = [&](int c) -> float {
             const int j = c - c0;
             if (rb) {
-                const float n = msg_n(at(nx, qb + j - d.pbase), p.l1, U(i, c));
+                const float n = msg_n(at(nx, qbp + j), p.l1, U(i, c));
                 if (!ra) return n;
                 const float m = msg_m(n, p.l2, kc.x, sc.t[c] - tb);
                 const bool cbc = sc.coinc[qb + j];

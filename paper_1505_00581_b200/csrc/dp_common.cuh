@@ -1,4 +1,4 @@
-// dp_common.cuh -- types shared by the K-DP / K-BT kernels (dp.cu, dp_tiled.cu).
+// dp_common.cuh -- types shared by the K-DP / K-BT kernels (dp.cu, dp_batch.cu, backtrack.cu).
 #pragma once
 #include "hgm_device.cuh"
 #include "hgm_internal.cuh"
@@ -16,6 +16,7 @@ struct SceneView {
     const int64_t *__restrict__ id;
     const int32_t *__restrict__ qpad;      // padded band (K-DP staging)
     const float *__restrict__ theta_pad;
+    const int32_t *__restrict__ prow_pad;  // row of each padded entry, -1 = padding slot
     const int32_t *__restrict__ rfc, *__restrict__ rlc;  // per-row first / last coincident column
     const int4 *__restrict__ ninfo;  // (t', minnode(t'+1), qstart, qpad) per node
     int fmax, S;
@@ -34,17 +35,15 @@ struct InstDesc {
     int64_t off;      // offset of this instance inside a layer
     int32_t out;      // output slot (offset index)
     int32_t o;        // first frame of the window
-    int64_t moff;     // offset of this instance's message rows in the message buffer (floats)
     int32_t ppad;     // padded band index of the window's first row = qpad[wb]
+    int32_t npp;      // padded pair slots of the window = qpad[we] - qpad[wb]
+    int32_t ntail;    // first dummy-form slot of a layer: np (v0, compact) or npp (padded layout)
     int32_t pad_;
 };
 
-// Message buffer layout (per instance, padded band order, model index fastest):
-//   msg[moff + (qpad[b] - ppad + j) * nm_pad(NM) + k] = m^k_i(b, c_j)
-// element stride of the message rows: aligned for LDS.64 / LDS.128 vector loads
-__host__ __device__ constexpr int nm_pad(int nm) {
-    return nm <= 1 ? 1 : nm <= 2 ? 2 : nm <= 4 ? 4 : nm <= 6 ? 6 : 8;
-}
+// K-DP shared-memory entry of a candidate (b, c_j): the NM messages m^k(b, c_j),
+// then theta(b -> c_j), padded to whole float4 (LDS.128) -- dp_batch.cu
+__host__ __device__ constexpr int entry_floats(int nm) { return ((nm + 1) + 3) & ~3; }
 
 struct StepConst {
     float g_i, g_im1, A1, K2;  // model gaps (Eq. 5) and angle constants (Eq. 6), hgm_device.cuh
@@ -55,18 +54,31 @@ struct DPParams {
     int T;
 };
 
-// Layer layout of one instance: [pairs np | (b,eps) Sw | (eps,a) Sw | (eps,eps) 1]
-__device__ __forceinline__ int ns_of(const InstDesc &d) { return d.np + 2 * (d.we - d.wb) + 1; }
+// Layer layout of one instance: [pairs | (b,eps) Sw | (eps,a) Sw | (eps,eps) 1], the
+// pairs compact (np slots, v0 kernels) or in padded band order (npp slots: state
+// (b, a) at qpad[a] - ppad + column of b in row a), model index fastest.
+__device__ __forceinline__ int ns_of(const InstDesc &d) { return d.ntail + 2 * (d.we - d.wb) + 1; }
 
-struct TileGeom {  // shared-memory capacities of one K-DP tile, upper bounds over the call
-    int FT;     // b-frames per tile
-    int NB;     // message rows (b nodes) per tile
-    int NA;     // direction rows (a and b nodes) per tile
-    int TH;     // floats of the padded direction rows
-    int MT;     // float2 of the padded message rows
-    int NST;    // real states per tile
+struct TileCaps {  // shared-memory capacities of one K-DP work item, maxima over the call's tiles
+    int NE;     // candidate entries (padded band slots of the tile's b rows)
+    int TH;     // floats of the padded direction rows [A0, B1) incl. alignment slack
+    int NA;     // direction rows (a and b nodes)
+    int NB;     // b nodes
+    int NC;     // candidate nodes [B0, Cend)
+    int NST;    // real states
+    int FT;     // b-frames
     int W;      // window length in frames
-    int ntile;  // tiles per window
+};
+
+// One K-DP work item: a tile of b-frames [F0, F1) of window `inst` (dp_batch.cu).
+struct WorkItem {
+    int inst, F0, F1;
+    int B0, B1;    // b nodes: minnode(F0), minnode(F1)
+    int A0;        // first direction row: max(minnode(F0 - T + 1), window start)
+    int Cend;      // candidate nodes end: min(minnode(F1 + T - 1), window end)
+    int qa, qb0, qb1;  // qpad[A0], qpad[B0], qpad[B1]
+    // filled by the prefetching thread: shared-memory index of each range's first element
+    int th0, araw0, we0, eb0, ee0, uc0, tc0, rf0, ft0, flo;
 };
 
 constexpr int MAX_BATCH = 8;  // models of equal M evaluated together by one CTA
@@ -85,6 +97,9 @@ struct BTArgs {
 
 struct StepConstB {  // per-model constants of one step, in the kernel parameter space
     float4 c[MAX_BATCH];  // (g_i, g_{i-1}, A1, K2)
+    // the same angle constants negated and paired for the packed (f32x2) candidate body:
+    // nA1[q] = (-A1_{2q}, -A1_{2q+1}), nK2[q] = (-K2_{2q}, -K2_{2q+1}) (odd batch: last pair repeats)
+    float2 nA1[MAX_BATCH / 2], nK2[MAX_BATCH / 2];
 };
 
 __device__ __forceinline__ float warp_min(float v) {

@@ -1,7 +1,7 @@
 // driver.cu -- host orchestration of one model batch at every offset:
-// window descriptors, tile geometry, chunking of the alpha history, one K-DP
-// launch per recursion step i = M..3 (Eq. 10, the paper's host loop of
-// Alg. 2 with the whole batch of windows per launch), then K-BT.
+// window descriptors, the frame tiling of K-DP's work items, chunking of the
+// alpha history, one K-DP launch per recursion step i = M..3 (Eq. 10, the
+// paper's host loop of Alg. 2 with the whole batch of windows per launch), then K-BT.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -10,13 +10,15 @@
 
 namespace hgm {
 
-hgm_status launch_dp_batch(int NM, const SceneView &v, const InstDesc *dinst, int ninst, float *hist, int64_t L,
-                           int layer, bool has_next, bool has_prev, const StepConstB &kc, const float *msg,
-                           const DPParams &p, const TileGeom &tg, cudaStream_t s);
-hgm_status launch_msg(int NM, const SceneView &v, const InstDesc *dinst, int ninst, int max_np, int max_sw,
-                      float *hist, int64_t L, int layer, bool has_next, bool init, const StepConstB &kc,
-                      const float *Ui, float *msg, const DPParams &p, int W, cudaStream_t s);
-size_t dp_batch_smem(const TileGeom &tg, int T, int NM);
+hgm_status launch_dp_batch(int NM, const SceneView &v, const InstDesc *dinst, const WorkItem *items, int nitems,
+                           int *counter, float *hist, int64_t L, int layer, bool has_next, bool has_prev,
+                           const StepConstB &kc, const float *U, int64_t ui_off, const DPParams &p,
+                           const TileCaps &caps, cudaStream_t s);
+hgm_status launch_items(const SceneView &v, const InstDesc *dinst, int ninst, int W, int T, const int32_t *gstart,
+                        const int32_t *tile_of, int tf_lo, int slots, WorkItem *items, cudaStream_t s);
+hgm_status launch_init_ee(const InstDesc *dinst, int ninst, float *hist, int64_t L, int layer, int NM,
+                          cudaStream_t s);
+size_t dp_batch_smem(const TileCaps &c, int T, int NM);
 hgm_status launch_backtrack_warp(const SceneView &v, const InstDesc *dinst, int ninst, const float *hist, int64_t L,
                                  const BTArgs &bt, const DPParams &p, cudaStream_t s);
 hgm_status launch_dp_v0(const SceneView &v, const InstDesc *dinst, int ninst, int64_t maxNs, float *hist, int64_t L,
@@ -46,49 +48,70 @@ bool use_v0_kernels() {
     return e && strcmp(e, "v0") == 0;
 }
 
-// Shared-memory capacities of a K-DP tile of FT b-frames, as upper bounds over
-// every tile start the call can produce (host, from the frame index); the
-// largest FT within the budget wins.
-static bool tile_geometry(const hgm_scene *sc, const hgm_offsets &o, int T, int NM, TileGeom *tg) {
-    const int64_t f_lo = (int64_t)o.first_frame - T - 1;
-    const int64_t f_hi = (int64_t)o.first_frame + (int64_t)(o.count - 1) * o.stride + o.window + T + 1;
-    auto Q = [&](int n) { return (int64_t)sc->qstart_h[n]; };
-    auto QP = [&](int n) { return (int64_t)sc->qpad_h[n]; };
-    static const int cand[] = {8, 6, 5, 4, 3, 2, 1};
-    const char *env = getenv("HGM_TILE_FRAMES");
-    const int want = env ? atoi(env) : 0;
-    for (int pass = 0; pass < 2; ++pass) {
-        for (int FT : cand) {
-            if (want > 0 && FT != want) continue;
-            if (FT * (T - 1) > 255) continue;  // segment ids are bytes
-            TileGeom g{};
-            g.FT = FT;
-            g.W = o.window;
-            g.ntile = (o.window + FT - 1) / FT;
-            int64_t NB = 1, NA = 1, TH = 1, MT = 1, NST = 1;
-            for (int64_t F0 = f_lo; F0 <= f_hi; ++F0) {
-                const int B0 = host_first(sc, F0), B1 = host_first(sc, F0 + FT), A0 = host_first(sc, F0 - T + 1);
-                NB = std::max<int64_t>(NB, B1 - B0);
-                NA = std::max<int64_t>(NA, B1 - A0);
-                TH = std::max<int64_t>(TH, QP(B1) - QP(A0) + 8);  // one aligned copy of the padded rows
-                MT = std::max<int64_t>(MT, QP(B1) - QP(B0) + 8);  // message rows, padded, + alignment slack
-                int64_t nst = 0;
-                for (int64_t f = F0; f < F0 + FT; ++f)
-                    nst += (int64_t)(host_first(sc, f + 1) - host_first(sc, f)) *
-                           (host_first(sc, f) - host_first(sc, f - T + 1));
-                NST = std::max(NST, nst);
-            }
-            g.NB = (int)NB;
-            g.NA = (int)NA;
-            g.TH = (int)TH;
-            g.MT = (int)MT;
-            g.NST = (int)NST;
-            const size_t budget = pass == 0 ? 60 * 1024 : 200 * 1024;
-            if (dp_batch_smem(g, T, NM) <= budget) {
-                *tg = g;
-                return true;
-            }
+// K-DP tiling: the frames [f_lo, f_hi) the call's windows cover are cut into tiles
+// of consecutive b-frames, greedily: a tile grows while the shared-memory footprint
+// of its two big buffers (candidate entries + raw alpha rows, 2 stages of direction
+// rows) stays under a cap; a single frame is always a tile.  A window's work items
+// are the tiles meeting its frames, clipped to them.  The kernel's shared-memory
+// plan is sized to the maxima over the tiles produced; the cap shrinks until the
+// plan fits the budget (2 CTAs per SM), else a 1-CTA-per-SM budget is tried.
+struct Tiling {
+    TileCaps caps{};
+    std::vector<int32_t> gstart;   // tile start frames, then f_hi, then sentinels
+    std::vector<int32_t> tile_of;  // tile index of frame f_lo + q
+    int f_lo = 0, slots = 1;
+};
+
+static bool make_tiling(const hgm_scene *sc, const hgm_offsets &o, int T, int NM, Tiling *tl) {
+    const int64_t f_lo = o.first_frame;
+    const int64_t f_hi = (int64_t)o.first_frame + (int64_t)(o.count - 1) * o.stride + o.window;
+    auto QP = [&](int64_t f) { return (int64_t)sc->qpad_h[host_first(sc, f)]; };
+    auto NF = [&](int64_t f) { return (int64_t)host_first(sc, f); };
+    const int FT_max = std::max(1, std::min(8, 255 / std::max(1, T - 1)));
+    const char *benv = getenv("HGM_SMEM_KB");  // tuning knob: shared memory per CTA (2 CTAs per SM by default)
+    const size_t budgets[2] = {(size_t)(benv ? atoi(benv) : 110) * 1024, 220 * 1024};
+    const int64_t ent_bytes = 4 * (entry_floats(NM) + NM);  // EN + raw alpha per candidate entry
+    for (int bi = 0; bi < 2; ++bi)
+    for (int64_t cap = (int64_t)budgets[bi]; cap >= 4096; cap = cap * 7 / 8) {
+        const size_t budget = budgets[bi];
+        Tiling t;
+        t.f_lo = (int)f_lo;
+        TileCaps c{1, 1, 1, 1, 1, 1, 1, o.window};
+        bool ok = true;
+        for (int64_t F0 = f_lo; F0 < f_hi;) {
+            int64_t F1 = F0 + 1;
+            auto ne = [&](int64_t a, int64_t b) { return QP(b) - QP(a); };
+            auto th = [&](int64_t a, int64_t b) { return QP(b) - QP(a - T + 1) + 8; };
+            auto foot = [&](int64_t a, int64_t b) { return ent_bytes * ne(a, b) + 8 * th(a, b); };
+            while (F1 < f_hi && F1 - F0 < FT_max && foot(F0, F1 + 1) <= cap) ++F1;
+            t.gstart.push_back((int32_t)F0);
+            c.NE = (int)std::max<int64_t>(c.NE, ne(F0, F1));
+            c.TH = (int)std::max<int64_t>(c.TH, th(F0, F1));
+            c.NA = (int)std::max<int64_t>(c.NA, NF(F1) - NF(F0 - T + 1));
+            c.NB = (int)std::max<int64_t>(c.NB, NF(F1) - NF(F0));
+            c.NC = (int)std::max<int64_t>(c.NC, NF(F1 + T - 1) - NF(F0));
+            int64_t nst = 0;
+            for (int64_t f = F0; f < F1; ++f) nst += (NF(f + 1) - NF(f)) * (NF(f) - NF(f - T + 1));
+            c.NST = (int)std::max<int64_t>(c.NST, nst);
+            c.FT = (int)std::max<int64_t>(c.FT, F1 - F0);
+            F0 = F1;
         }
+        if (!ok || dp_batch_smem(c, T, NM) > budget) continue;
+        const int ntiles = (int)t.gstart.size();
+        t.gstart.push_back((int32_t)f_hi);
+        t.tile_of.resize((size_t)(f_hi - f_lo));
+        for (int q = 0; q < ntiles; ++q)
+            for (int64_t f = t.gstart[q]; f < t.gstart[q + 1]; ++f) t.tile_of[f - f_lo] = q;
+        int slots = 1;
+        for (int k = 0; k < o.count; ++k) {
+            const int64_t of = (int64_t)o.first_frame + (int64_t)k * o.stride;
+            slots = std::max(slots, t.tile_of[of + o.window - 1 - f_lo] - t.tile_of[of - f_lo] + 1);
+        }
+        for (int q = 0; q <= slots; ++q) t.gstart.push_back(INT32_MAX / 2);  // slots past the last tile: empty
+        t.slots = slots;
+        t.caps = c;
+        *tl = std::move(t);
+        return true;
     }
     return false;
 }
@@ -111,13 +134,25 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
         d.we = host_first(sc, of + o.window);
         d.pbase = sc->qstart_h[d.wb];
         d.np = sc->qstart_h[d.we] - sc->qstart_h[d.wb];
+        d.ppad = sc->qpad_h[d.wb];
+        d.npp = sc->qpad_h[d.we] - sc->qpad_h[d.wb];
+        d.ntail = v0 ? d.np : d.npp;  // v0 kernels: compact pair layout
         d.out = k;
         d.o = (int32_t)of;
         all[k] = d;
     }
-    TileGeom tg{};
-    if (!v0 && !tile_geometry(sc, o, pp.T, NM, &tg))
-        return fail(HGM_ERR_INVALID_ARGUMENT, "window too dense for the shared-memory tile (reduce T or window)");
+    Tiling tl;
+    if (!v0 && !make_tiling(sc, o, pp.T, NM, &tl))
+        return fail(HGM_ERR_INVALID_ARGUMENT, "frames too dense for the shared-memory tile (reduce T or window)");
+    DevBuf d_gstart, d_tile_of;
+    if (!v0) {
+        HGM_TRY(d_gstart.alloc(sizeof(int32_t) * tl.gstart.size(), s));
+        HGM_TRY(d_tile_of.alloc(sizeof(int32_t) * std::max<size_t>(1, tl.tile_of.size()), s));
+        HGM_CUDA(cudaMemcpyAsync(d_gstart.p, tl.gstart.data(), sizeof(int32_t) * tl.gstart.size(),
+                                 cudaMemcpyHostToDevice, s));
+        HGM_CUDA(cudaMemcpyAsync(d_tile_of.p, tl.tile_of.data(), sizeof(int32_t) * tl.tile_of.size(),
+                                 cudaMemcpyHostToDevice, s));
+    }
     DPParams p;
     p.l1 = pp.lambda1;
     p.l2 = pp.lambda2;
@@ -125,13 +160,13 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
     p.W = pp.w_dummy;
     p.l1W = pp.lambda1 * pp.w_dummy;
     p.T = pp.T;
-    const SceneView v{sc->t,    sc->first_tab, sc->qstart, sc->theta,     sc->coinc, sc->cpre,
-                      sc->prow, sc->id,        sc->qpad,   sc->theta_pad, sc->rfc,   sc->rlc,
-                      sc->ninfo, sc->fmax,     (int)sc->S};
+    const SceneView v{sc->t,    sc->first_tab, sc->qstart,    sc->theta,    sc->coinc, sc->cpre,
+                      sc->prow, sc->id,        sc->qpad,      sc->theta_pad, sc->prow_pad, sc->rfc,
+                      sc->rlc,  sc->ninfo,     sc->fmax,      (int)sc->S};
     const int nsteps = M >= 3 ? M - 2 : 0;
     // Windows are processed in chunks (the alpha history of a chunk must fit the
-    // budget).  Chunks alternate between two streams, so the streaming K-MSG of
-    // one chunk overlaps the compute-bound K-DP of the other on the same SMs.
+    // budget; a smaller chunk keeps a layer L2-resident for the next step's reads).
+    // Optionally chunks alternate between two streams.
     const int64_t budget_floats = (int64_t)3 << 29;  // alpha history per chunk: 6 GiB
     BTArgs bt{};
     bt.U = U;
@@ -145,15 +180,14 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
         bt.A[k] = outs[k].A;
         bt.z[k] = outs[k].z;
     }
-    const int NMP = nm_pad(NM);
     const char *cenv = getenv("HGM_CHUNK");  // windows per chunk (tuning knob)
     const int chunk_max = std::min(65535, cenv && atoi(cenv) > 0 ? atoi(cenv) : 4096);
     const char *senv = getenv("HGM_STREAMS");  // 2: alternate chunks over two streams (measured slower)
     const int nlanes = (senv && atoi(senv) == 2) ? 2 : 1;
     struct Lane {
         cudaStream_t s = nullptr;
-        DevBuf hist, msg, dinst;
-        int64_t hist_cap = 0, msg_cap = 0, dinst_cap = 0;
+        DevBuf hist, dinst, items, counters;
+        int64_t hist_cap = 0, dinst_cap = 0, items_cap = 0, counters_cap = 0;
     } lanes[2];
     lanes[0].s = s;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -169,20 +203,15 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
     for (int k0 = 0; k0 < count && st == HGM_OK; ++chunk) {
         Lane &ln = lanes[chunk % nlanes];
         const cudaStream_t ls = ln.s;
-        int64_t L = 0, maxNs = 1, MS = 0;
-        int k1 = k0, max_sw = 1, max_np = 1;
+        int64_t L = 0, maxNs = 1;
+        int k1 = k0;
         while (k1 < count && k1 - k0 < chunk_max) {
             InstDesc &d = all[k1];
-            const int64_t ns = (int64_t)d.np + 2 * (int64_t)(d.we - d.wb) + 1;
+            const int64_t ns = (int64_t)d.ntail + 2 * (int64_t)(d.we - d.wb) + 1;
             if (k1 > k0 && (L + ns * NM) * std::max(nsteps, 1) > budget_floats) break;
             d.off = L;
             L += ns * NM;
-            d.ppad = sc->qpad_h[d.wb];
-            d.moff = MS;
-            MS += (((int64_t)sc->qpad_h[d.we] - d.ppad) * NMP + 3) & ~(int64_t)3;  // 16-byte aligned rows
             maxNs = std::max(maxNs, ns);
-            max_sw = std::max(max_sw, d.we - d.wb);
-            max_np = std::max(max_np, d.np);
             ++k1;
         }
         const int ninst = k1 - k0;
@@ -196,18 +225,29 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
             st = cuda_fail(e, "cudaMemcpyAsync(instances)");
             break;
         }
-        const int64_t need = L * nsteps;
+        const int64_t need = L * nsteps + 4;  // + 16 bytes: K-DP's bulk copies round ranges to 16-byte units
         if (need > ln.hist_cap) {
             if ((st = ln.hist.alloc(sizeof(float) * need, ls)) != HGM_OK) break;
             ln.hist_cap = need;
         }
-        if (!v0 && nsteps > 0 && MS + 4 > ln.msg_cap) {
-            if ((st = ln.msg.alloc(sizeof(float) * (MS + 4), ls)) != HGM_OK) break;
-            ln.msg_cap = MS + 4;
-        }
         const InstDesc *di = ln.dinst.as<InstDesc>();
         float *hist = ln.hist.as<float>();
-        auto Urow = [&](int i) { return U + ((int64_t)i * nn - n_lo) * NM; };  // batched row, Urow(i)[c*NM + k]
+        const int nitems = ninst * tl.slots;
+        if (!v0 && nsteps > 0) {
+            if (nitems > ln.items_cap) {
+                if ((st = ln.items.alloc(sizeof(WorkItem) * nitems, ls)) != HGM_OK) break;
+                ln.items_cap = nitems;
+            }
+            if (nsteps > ln.counters_cap) {
+                if ((st = ln.counters.alloc(sizeof(int) * nsteps, ls)) != HGM_OK) break;
+                ln.counters_cap = nsteps;
+            }
+            HGM_CUDA(cudaMemsetAsync(ln.counters.p, 0, sizeof(int) * nsteps, ls));
+            launch_items(v, di, ninst, o.window, p.T, d_gstart.as<int32_t>(), d_tile_of.as<int32_t>(), tl.f_lo,
+                         tl.slots, ln.items.as<WorkItem>(), ls);
+            launch_init_ee(di, ninst, hist, L, nsteps - 1, NM, ls);  // first layer's (eps, eps) slots
+            count_launch(K_DP, 2);
+        }
         for (int i = M - 1; i >= 2 && st == HGM_OK; --i) {
             const bool has_next = i + 1 <= M - 1;
             if (v0) {
@@ -220,17 +260,16 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
             }
             StepConstB kc{};
             for (int k = 0; k < NM; ++k) kc.c[k] = models[k]->step_h[i];
-            {
-                Timer tm(ls, K_MSG);
-                st = launch_msg(NM, v, di, ninst, max_np, max_sw, hist, L, i - 2, has_next, /*init=*/!has_next, kc,
-                                Urow(i), ln.msg.as<float>(), p, o.window, ls);
-                count_launch(K_MSG, has_next ? 1 : 2);
+            for (int q = 0; q < (NM + 1) / 2; ++q) {
+                const int k1 = std::min(2 * q + 1, NM - 1);
+                kc.nA1[q] = make_float2(-kc.c[2 * q].z, -kc.c[k1].z);
+                kc.nK2[q] = make_float2(-kc.c[2 * q].w, -kc.c[k1].w);
             }
-            if (st != HGM_OK) break;
             {
                 Timer tm(ls, K_DP);
-                st = launch_dp_batch(NM, v, di, ninst, hist, L, i - 2, has_next, /*has_prev=*/i - 1 >= 2, kc,
-                                     ln.msg.as<float>(), p, tg, ls);
+                st = launch_dp_batch(NM, v, di, ln.items.as<WorkItem>(), nitems, ln.counters.as<int>() + (i - 2), hist,
+                                     L, i - 2, has_next, /*has_prev=*/i - 1 >= 2, kc, U,
+                                     ((int64_t)i * nn - n_lo) * NM, p, tl.caps, ls);
                 count_launch(K_DP);
             }
         }

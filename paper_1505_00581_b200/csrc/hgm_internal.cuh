@@ -85,6 +85,7 @@ struct hgm_scene {
     // tile's rows [A0, B1) are copied as ONE contiguous range
     int32_t *qpad = nullptr;    // [S + 1]
     float *theta_pad = nullptr; // [qpad[S]]
+    int32_t *prow_pad = nullptr; // [qpad[S]]: row a of each padded entry, -1 for a padding slot
     int32_t *rfc = nullptr;     // [S]: first coincident column of row a (INT_MAX if none)
     int32_t *rlc = nullptr;     // [S]: last coincident column of row a (-1 if none)
     int4 *ninfo = nullptr;      // [S]: (t'(x), minnode(t'(x)+1), qstart[x], qpad[x]) -- one load per row

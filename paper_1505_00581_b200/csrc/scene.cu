@@ -74,7 +74,7 @@ __global__ void k_padlen(int64_t S, const int32_t *__restrict__ rowlen, int32_t 
 __global__ void k_band(int64_t S, int T_max, int fmax, const int32_t *__restrict__ t, const float *__restrict__ x,
                        const float *__restrict__ y, const int32_t *__restrict__ ft, const int32_t *__restrict__ qstart,
                        const int32_t *__restrict__ qpad, float *theta, float *theta_pad, uint8_t *coinc,
-                       uint16_t *cpre, int32_t *prow, int32_t *rfc, int32_t *rlc) {
+                       uint16_t *cpre, int32_t *prow, int32_t *prow_pad, int32_t *rfc, int32_t *rlc) {
     int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (a >= S) return;
     int lo = first_at(ft, fmax, (int)S, t[a] + 1);
@@ -82,6 +82,7 @@ __global__ void k_band(int64_t S, int T_max, int fmax, const int32_t *__restrict
     float ax = x[a], ay = y[a];
     int64_t p = qstart[a];
     float *tp = theta_pad + qpad[a];
+    int32_t *rp = prow_pad + qpad[a];
     unsigned run = 0;
     int fc = 0x7fffffff, lc = -1;
     for (int c = lo; c < hi; ++c, ++p) {
@@ -90,6 +91,7 @@ __global__ void k_band(int64_t S, int T_max, int fmax, const int32_t *__restrict
         const float th = dir_of(ax, ay, cx, cy);
         theta[p] = th;
         tp[c - lo] = th;
+        rp[c - lo] = (int32_t)a;
         coinc[p] = co ? 1 : 0;
         run += co ? 1u : 0u;
         cpre[p] = (uint16_t)min(run, 65535u);
@@ -99,7 +101,10 @@ __global__ void k_band(int64_t S, int T_max, int fmax, const int32_t *__restrict
             lc = c - lo;
         }
     }
-    if (((hi - lo) & 1) == 0) tp[hi - lo] = 0.f;  // padding slot
+    if (((hi - lo) & 1) == 0) {  // padding slot
+        tp[hi - lo] = 0.f;
+        rp[hi - lo] = -1;
+    }
     rfc[a] = fc;
     rlc[a] = lc;
 }
@@ -130,7 +135,7 @@ static hgm_status sort_by_frame(const int32_t *frame, int64_t n, int32_t *keys_o
 static void free_scene_dev(hgm_scene *sc) {
     void *ptrs[] = {sc->t,      sc->x,     sc->y,     sc->feat, sc->id,  sc->first_tab,
                     sc->qstart, sc->theta, sc->coinc, sc->cpre, sc->prow,
-                    sc->qpad,   sc->theta_pad, sc->rfc, sc->rlc, sc->ninfo};
+                    sc->qpad,   sc->theta_pad, sc->prow_pad, sc->rfc, sc->rlc, sc->ninfo};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -156,7 +161,7 @@ hgm_status scene_build_device(const hgm_points *pts, int32_t T_max, cudaStream_t
         cudaError_t e__ = (call);                                        \
         if (e__ != cudaSuccess) return bail(cuda_fail(e__, #call));      \
     } while (0)
-    SC_CUDA(dmalloc(&sc->t, sizeof(int32_t) * n));
+    SC_CUDA(dmalloc(&sc->t, sizeof(int32_t) * (n + 4)));  // + 16 B slack on arrays K-DP bulk-copies
     SC_CUDA(dmalloc(&sc->x, sizeof(float) * n));
     SC_CUDA(dmalloc(&sc->y, sizeof(float) * n));
     SC_CUDA(dmalloc(&sc->feat, sizeof(float) * n * sc->Fp));
@@ -179,7 +184,7 @@ hgm_status scene_build_device(const hgm_points *pts, int32_t T_max, cudaStream_t
     SC_CUDA(cudaStreamSynchronize(s));
     if (tt[0] < 0) return bail(fail(HGM_ERR_INVALID_ARGUMENT, "negative frame index"));
     sc->fmax = tt[1];
-    SC_CUDA(dmalloc(&sc->first_tab, sizeof(int32_t) * (sc->fmax + 2)));
+    SC_CUDA(dmalloc(&sc->first_tab, sizeof(int32_t) * (sc->fmax + 2 + 4)));
     k_first_tab<<<(unsigned)((n + 1 + 255) / 256), 256, 0, s>>>(n, sc->t, sc->first_tab);
     DevBuf rowlen, tmp;
     if (rowlen.alloc(sizeof(int32_t) * (n + 1), s) != HGM_OK) return bail(HGM_ERR_OUT_OF_MEMORY);
@@ -209,9 +214,10 @@ hgm_status scene_build_device(const hgm_points *pts, int32_t T_max, cudaStream_t
     SC_CUDA(cudaStreamSynchronize(s));
     sc->npairs = sc->qstart_h[n];
     if (sc->qpad_h[n] < sc->npairs) return bail(fail(HGM_ERR_INVALID_ARGUMENT, "pair band exceeds 2^31 entries"));
-    SC_CUDA(dmalloc(&sc->rfc, sizeof(int32_t) * n));
-    SC_CUDA(dmalloc(&sc->rlc, sizeof(int32_t) * n));
+    SC_CUDA(dmalloc(&sc->rfc, sizeof(int32_t) * (n + 4)));
+    SC_CUDA(dmalloc(&sc->rlc, sizeof(int32_t) * (n + 4)));
     SC_CUDA(dmalloc(&sc->theta_pad, sizeof(float) * ((int64_t)sc->qpad_h[n] + 4)));
+    SC_CUDA(dmalloc(&sc->prow_pad, sizeof(int32_t) * ((int64_t)sc->qpad_h[n] + 4)));
     if (sc->npairs > 0) {
         SC_CUDA(dmalloc(&sc->theta, sizeof(float) * sc->npairs));
         SC_CUDA(dmalloc(&sc->coinc, sizeof(uint8_t) * sc->npairs));
@@ -220,7 +226,7 @@ hgm_status scene_build_device(const hgm_points *pts, int32_t T_max, cudaStream_t
     }
     k_band<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(n, T_max, sc->fmax, sc->t, sc->x, sc->y, sc->first_tab,
                                                        sc->qstart, sc->qpad, sc->theta, sc->theta_pad, sc->coinc,
-                                                       sc->cpre, sc->prow, sc->rfc, sc->rlc);
+                                                       sc->cpre, sc->prow, sc->prow_pad, sc->rfc, sc->rlc);
     SC_CUDA(dmalloc(&sc->ninfo, sizeof(int4) * n));
     k_ninfo<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, sc->fmax, sc->t, sc->first_tab, sc->qstart, sc->qpad,
                                                         sc->ninfo);
