@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(128) k_backtrack_warp(SceneView sc, const Inst
     auto layer = [&](int i) -> const float * {
         return (i >= 2 && i <= M - 1) ? hist + (int64_t)(i - 2) * L + d.off : nullptr;
     };
-    auto at = [&](const float *l, int s) { return l ? l[(int64_t)s * NM + kk] : 0.f; };
+    auto at = [&](const float *l, int s) { return l ? l[(int64_t)s * bt.SS + kk] : 0.f; };  // state stride SS
     // layer layout (dp_common.cuh): pair state (later, earlier) at qpad[earlier] - ppad + column
     auto a_be = [&](const float *l, int b) { return at(l, d.ntail + (b - d.wb)); };
     auto a_ea = [&](const float *l, int a) { return at(l, d.ntail + Sw + (a - d.wb)); };

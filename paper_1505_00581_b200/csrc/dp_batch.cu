@@ -38,6 +38,9 @@
 //
 // The arithmetic is hgm_device.cuh's (packed ops round like the scalar ones), so the
 // backtrack's re-evaluation (backtrack.cu) stays bit-identical.
+#include <cstdio>
+#include <cstdlib>
+
 #include "dp_common.cuh"
 
 namespace hgm {
@@ -53,14 +56,41 @@ struct Seg {  // one (b-frame f, a-frame f-g) block of real states
     unsigned inv;  // ceil(2^32 / nb): division-free state decode
 };
 
-constexpr int KDP_THREADS = 256;
+constexpr int KDP_THREADS = 256;               // compute warps
 constexpr int KDP_WARPS = KDP_THREADS / 32;
+constexpr int KDP_BLOCK = KDP_THREADS + 32;      // + one copy warp (claims items, issues their TMA copies)
 constexpr int NROWI = 6;  // derived row bookkeeping ints per row
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
+// Per-item bookkeeping that does not change from step to step (computed once per
+// chunk by k_item_prep, copied into the stage with the item's other inputs):
+//   nst | segments (with prefix starts) | row tables | state -> segment map
+struct BookPlan {
+    size_t nst, seg, rows, map, total;
+    __host__ __device__ BookPlan(const TileCaps &c, int T) {
+        size_t o = 0;
+        auto take = [&](size_t bytes) {
+            const size_t r = o;
+            o = align16(o + bytes);
+            return r;
+        };
+        nst = take(16);
+        seg = take(sizeof(Seg) * (size_t)c.FT * (T - 1));
+        rows = take(sizeof(int) * NROWI * (size_t)c.NA);
+        map = take((size_t)c.NST);
+        total = o;
+    }
+};
+
+// Shared memory: two STAGES, each the TMA target of one work item (its candidate
+// entries -- the alpha_{i+1} rows land there in the layer's own layout and become
+// messages in place --, its direction rows and its small raw inputs), plus the
+// bookkeeping of the item being processed (rows, segments, state map, dummy terms).
+// While one item is processed the copies of the next one land in the other stage.
 struct SmemPlan {
-    size_t en, araw, th0, th1, uc, we, tc, ni, rfc, rlc, eb, ee, ftab, rows, bean, fw, dl, seg, map, item, total;
+    size_t en[2], th[2], uc[2], we[2], tc[2], ni[2], eb[2], ee[2], ftab[2], bk[2];
+    size_t bean, fw, dl, ctl, total;
     __host__ __device__ SmemPlan(const TileCaps &c, int T, int NM) {
         size_t o = 0;
         auto take = [&](size_t bytes) {
@@ -68,26 +98,23 @@ struct SmemPlan {
             o = align16(o + bytes);
             return r;
         };
-        en = take(sizeof(float) * (size_t)entry_floats(NM) * c.NE);
-        araw = take(sizeof(float) * ((size_t)NM * c.NE + 8));
-        th0 = take(sizeof(float) * ((size_t)c.TH + 8));
-        th1 = take(sizeof(float) * ((size_t)c.TH + 8));
-        uc = take(sizeof(float) * ((size_t)NM * c.NC + 8));
-        we = take(sizeof(float) * ((size_t)NM * c.NC + 8));
-        tc = take(sizeof(int) * ((size_t)c.NC + 8));
-        ni = take(sizeof(int4) * ((size_t)c.NA + 1));
-        rfc = take(sizeof(int) * ((size_t)c.NA + 8));
-        rlc = take(sizeof(int) * ((size_t)c.NA + 8));
-        eb = take(sizeof(float) * ((size_t)NM * c.NB + 8));
-        ee = take(sizeof(float) * ((size_t)NM + 8));
-        ftab = take(sizeof(int) * ((size_t)c.FT + 2 * T + 16));
-        rows = take(sizeof(int) * NROWI * (size_t)c.NA);
+        const int EPF = entry_floats(NM);
+        for (int s = 0; s < 2; ++s) {
+            en[s] = take(sizeof(float) * (size_t)EPF * c.NE);
+            th[s] = take(sizeof(float) * ((size_t)c.TH + 8));
+            uc[s] = take(sizeof(float) * ((size_t)NM * c.NC + 8));
+            we[s] = take(sizeof(float) * ((size_t)EPF * c.NC + 8));
+            tc[s] = take(sizeof(int) * ((size_t)c.NC + 8));
+            ni[s] = take(sizeof(int4) * ((size_t)c.NA + 1));
+            bk[s] = take(BookPlan(c, T).total);
+            eb[s] = take(sizeof(float) * ((size_t)EPF * c.NB + 8));
+            ee[s] = take(sizeof(float) * ((size_t)EPF + 8));
+            ftab[s] = take(sizeof(int) * ((size_t)c.FT + 2 * T + 16));
+        }
         bean = take(sizeof(float) * (size_t)NM * c.NB);
         fw = take(sizeof(float) * (size_t)NM * (c.FT + T));
         dl = take(sizeof(float) * (size_t)NM * T);
-        seg = take(sizeof(Seg) * (size_t)c.FT * (T - 1));
-        map = take((size_t)c.NST);
-        item = take(2 * sizeof(WorkItem) + 2 * sizeof(InstDesc) + 5 * 8 + 16);  // descriptors, mbarriers, scalars
+        ctl = take(512);  // item descriptors, mbarriers, counters
         total = o;
     }
 };
@@ -101,15 +128,19 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+// Spin on test_wait (never suspends: a suspended try_wait was seen to oversleep the
+// phase completion by up to milliseconds); the spin is a few instructions per probe.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
     unsigned ok = 0;
-    do {
+    for (;;) {
         asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
             : "=r"(ok)
             : "r"(smem_u32(bar)), "r"(parity)
             : "memory");
-    } while (!ok);
+        if (ok) break;
+        __nanosleep(32);
+    }
 }
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -118,21 +149,18 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
                  : "memory");
 }
 
-// Up to 12 bulk copies of one item, collected first so the mbarrier is armed with
-// the total byte count before any copy is issued.
-struct CopyList {
-    int n = 0;
+// Bulk copies into one mbarrier's phase: each copy first raises the phase's expected
+// transaction count (mbarrier.expect_tx, no arrival), then one arrival closes the
+// phase's arrival count once every copy is issued.
+struct Copier {
+    uint64_t *bar;
     unsigned total = 0;
-    void *dst[12];
-    const void *src[12];
-    unsigned bytes[12];
-    __device__ __forceinline__ void add(void *d, const void *s, unsigned b) {
-        if (b == 0) return;
-        dst[n] = d;
-        src[n] = s;
-        bytes[n] = b;
-        total += b;
-        ++n;
+    __device__ __forceinline__ explicit Copier(uint64_t *b) : bar(b) {}
+    __device__ __forceinline__ void raw(void *d, const void *s, unsigned bytes) {
+        if (bytes == 0) return;
+        asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+        bulk_g2s(d, s, bytes, bar);
+        total += bytes;
     }
     // Elements [g0, g1) of a 4-byte-element array, widened to whole 16-byte units
     // (the allocations carry >= 16 bytes of slack): dst[q] = src[a0 + q], a0 = g0 & ~3.
@@ -141,12 +169,11 @@ struct CopyList {
     __device__ __forceinline__ int range(void *d, const T *s, int64_t g0, int64_t g1) {
         static_assert(sizeof(T) == 4, "4-byte elements");
         const int64_t a0 = g0 & ~(int64_t)3, a1 = (g1 + 3) & ~(int64_t)3;
-        if (g1 > g0) add(d, s + a0, (unsigned)((a1 - a0) * 4));
+        if (g1 > g0) raw(d, s + a0, (unsigned)((a1 - a0) * 4));
         return (int)(g0 - a0);
     }
-    __device__ __forceinline__ void issue(uint64_t *bar) {
-        mbar_expect_tx(bar, total);
-        for (int q = 0; q < n; ++q) bulk_g2s(dst[q], src[q], bytes[q], bar);
+    __device__ __forceinline__ void close() {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
     }
 };
 
@@ -205,231 +232,198 @@ __device__ __forceinline__ void cand_values(float fb, float fc, const float *m, 
     }
 }
 
-// The bulk copies of one item's inputs (producer lane): every range is computed
-// first, the item's descriptors are published to shared memory, then the stage's
-// mbarrier is armed with the byte total and the copies are issued.
-template <int NM, bool kHasNext>
-__device__ __forceinline__ void plan_item(const SceneView &sc, WorkItem &w, const InstDesc &d, const float *hist,
-                                          int64_t L, int layer, const float *__restrict__ U, int64_t ui_off, int T,
-                                          const SmemPlan &sp, unsigned char *smem, int thstage, CopyList &cl) {
-    // sources are addressed from the (16-byte aligned) allocation bases
-    const int64_t nxo = (int64_t)(layer + 1) * L + d.off;  // alpha layer i+1 of this window in hist
-    const int Sw = d.we - d.wb;
-    // direction rows x in [A0, B1) of the padded band
-    w.th0 = w.qa - cl.range(smem + (thstage ? sp.th1 : sp.th0), sc.theta_pad, w.qa, w.qb1);  // TH[q] = theta_pad[th0 + q]
-    if (kHasNext) {  // alpha_{i+1}: rows of the tile's b nodes (padded layout) and the dummy-form slots
-        w.araw0 = cl.range(smem + sp.araw, hist, nxo + (int64_t)(w.qb0 - d.ppad) * NM, nxo + (int64_t)(w.qb1 - d.ppad) * NM);
-        w.we0 = cl.range(smem + sp.we, hist, nxo + (int64_t)(d.ntail + w.B0 - d.wb) * NM,
-                         nxo + (int64_t)(d.ntail + w.Cend - d.wb) * NM);
-        w.eb0 = cl.range(smem + sp.eb, hist, nxo + (int64_t)(d.ntail + Sw + w.B0 - d.wb) * NM,
-                         nxo + (int64_t)(d.ntail + Sw + w.B1 - d.wb) * NM);
-        w.ee0 = cl.range(smem + sp.ee, hist, nxo + (int64_t)(d.ntail + 2 * Sw) * NM,
-                         nxo + (int64_t)(d.ntail + 2 * Sw + 1) * NM);
-    }
-    w.uc0 = cl.range(smem + sp.uc, U, ui_off + (int64_t)w.B0 * NM, ui_off + (int64_t)w.Cend * NM);
-    w.tc0 = cl.range(smem + sp.tc, sc.t, w.B0, w.Cend);
-    if (w.B1 > w.A0) cl.add(smem + sp.ni, sc.ninfo + w.A0, (unsigned)(sizeof(int4) * (w.B1 - w.A0)));
-    w.rf0 = cl.range(smem + sp.rfc, sc.rfc, w.A0, w.B1);
-    cl.range(smem + sp.rlc, sc.rlc, w.A0, w.B1);
-    // first_tab over frames [F0 - T, F1 + T], clamped to the table
-    const int f_lo = max(0, w.F0 - T), f_hi = min(sc.fmax + 1, w.F1 + T);
-    w.ft0 = cl.range(smem + sp.ftab, sc.ft, f_lo, f_hi + 1);
-    w.flo = f_lo;
-}
-
+// mbarrier helpers beyond the TMA ones
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-// consumer-only barrier (the producer warp never joins it)
-__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(KDP_THREADS) : "memory"); }
+__device__ __forceinline__ void mbar_expect_tx_noarrive(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+// Optional pipeline trace (HGM_TRACE=1): globaltimer stamps of CTA 0, one launch.
+__device__ unsigned long long *g_trace = nullptr;
+__device__ __forceinline__ void trace(int m, int ev) {
+    if (g_trace && blockIdx.x == 0 && m < 64) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_trace[m * 8 + ev] = t;
+    }
+}
+
+// Control block in shared memory.
+struct Ctl {
+    WorkItem w[2];      // stage descriptors (w[s].live == 0: no more items)
+    int nst[2];         // real states of the current item
+    int claim[2];       // next unclaimed 32-state group
+    uint64_t raw[2];    // stage inputs landed (copy-warp arrival + TMA bytes)
+    uint64_t free_[2];  // stage released by the compute warps
+};
+
+// barrier of the compute warps only (the copy warp never joins it)
+__device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 1, %0;" ::"n"(KDP_THREADS) : "memory"); }
+
+// Issue the input copies of item (w, d) into stage s (producer lane 0): the alpha_{i+1}
+// rows of the tile's b nodes straight into the candidate-entry area (the layer's state
+// stride is the entry stride, so entry e = state slot qb0 - ppad + e), the direction
+// rows, and the small ranges of the dummy-form slots, the unary row, the scene index.
+template <int NM, bool kHasNext>
+__device__ __forceinline__ void issue_stage(const SceneView &sc, WorkItem &w, const float *hist,
+                                            int64_t L, int layer, const float *__restrict__ U, int64_t ui_off, int T,
+                                            const SmemPlan &sp, unsigned char *smem, int s, uint64_t *bar,
+                                            const unsigned char *__restrict__ book, unsigned book_bytes) {
+    constexpr int EPF = entry_floats(NM);
+    const InstDesc &d = w.d;
+    Copier cl(bar);
+    const int64_t nxo = (int64_t)(layer + 1) * L + d.off;  // alpha layer i+1 of this window (from the aligned base)
+    const int Sw = d.we - d.wb;
+    if (kHasNext) {
+        cl.range(smem + sp.en[s], hist, nxo + (int64_t)(w.qb0 - d.ppad) * EPF, nxo + (int64_t)(w.qb1 - d.ppad) * EPF);
+        w.we0 = cl.range(smem + sp.we[s], hist, nxo + (int64_t)(d.ntail + w.B0 - d.wb) * EPF,
+                         nxo + (int64_t)(d.ntail + w.Cend - d.wb) * EPF);
+        w.eb0 = cl.range(smem + sp.eb[s], hist, nxo + (int64_t)(d.ntail + Sw + w.B0 - d.wb) * EPF,
+                         nxo + (int64_t)(d.ntail + Sw + w.B1 - d.wb) * EPF);
+        w.ee0 = cl.range(smem + sp.ee[s], hist, nxo + (int64_t)(d.ntail + 2 * Sw) * EPF,
+                         nxo + (int64_t)(d.ntail + 2 * Sw + 1) * EPF);
+    }
+    w.th0 = w.qa - cl.range(smem + sp.th[s], sc.theta_pad, w.qa, w.qb1);  // TH[q] holds theta_pad[th0 + q]
+    w.uc0 = cl.range(smem + sp.uc[s], U, ui_off + (int64_t)w.B0 * NM, ui_off + (int64_t)w.Cend * NM);
+    w.tc0 = cl.range(smem + sp.tc[s], sc.t, w.B0, w.Cend);
+    if (w.B1 > w.A0) cl.raw(smem + sp.ni[s], sc.ninfo + w.A0, (unsigned)(sizeof(int4) * (w.B1 - w.A0)));
+    cl.raw(smem + sp.bk[s], book + (size_t)w.idx * book_bytes, book_bytes);  // the item's bookkeeping
+    const int f_lo = max(0, w.F0 - T), f_hi = min(sc.fmax + 1, w.F1 + T);  // first_tab over [F0 - T, F1 + T]
+    w.ft0 = cl.range(smem + sp.ftab[s], sc.ft, f_lo, f_hi + 1);
+    w.flo = f_lo;
+    cl.close();  // (the stage was released by the consumers' empty[s] arrivals, after their reads)
+}
 
 template <int NM, bool kHasNext>
-__global__ void __launch_bounds__(KDP_THREADS + 32, 2) k_dp_fused(SceneView sc, const InstDesc *__restrict__ inst,
-                                                             const WorkItem *__restrict__ items, int nitems,
-                                                             int *__restrict__ counter, float *__restrict__ hist,
-                                                             int64_t L, int layer, int has_prev, StepConstB kc,
-                                                             const float *__restrict__ U, int64_t ui_off, DPParams p,
-                                                             TileCaps caps) {
+__global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const WorkItem *__restrict__ items,
+                                                             int nitems, int *__restrict__ counter,
+                                                             float *__restrict__ hist, int64_t L, int layer,
+                                                             int has_prev, StepConstB kc, const float *__restrict__ U,
+                                                             int64_t ui_off, DPParams p, TileCaps caps,
+                                                             const unsigned char *__restrict__ book) {
     constexpr int EPF = entry_floats(NM);
     extern __shared__ __align__(128) unsigned char smem[];
     const SmemPlan sp(caps, p.T, NM);
-    float *EN = reinterpret_cast<float *>(smem + sp.en);
-    const float *ARAW = reinterpret_cast<const float *>(smem + sp.araw);
-    const float *UC = reinterpret_cast<const float *>(smem + sp.uc);
-    const float *WE = reinterpret_cast<const float *>(smem + sp.we);
-    const int *TC = reinterpret_cast<const int *>(smem + sp.tc);
-    const int4 *NI = reinterpret_cast<const int4 *>(smem + sp.ni);
-    const int *RFC = reinterpret_cast<const int *>(smem + sp.rfc);
-    const int *RLC = reinterpret_cast<const int *>(smem + sp.rlc);
-    const float *EB = reinterpret_cast<const float *>(smem + sp.eb);
-    const float *EE = reinterpret_cast<const float *>(smem + sp.ee);
-    const int *FTAB = reinterpret_cast<const int *>(smem + sp.ftab);
-    int *r_ofs = reinterpret_cast<int *>(smem + sp.rows);  // [NA] offset of row x in TH
-    int *r_en = r_ofs + caps.NA;                             // entry index of row x's column 0 in EN
-    int *r_q = r_en + caps.NA;                               // qstart[x] (compact band: coincidence flags)
-    int *r_qp = r_q + caps.NA;                               // qpad[x] (padded band: alpha slots)
-    int *r_fc = r_qp + caps.NA;                              // first / last coincident column
-    int *r_lc = r_fc + caps.NA;
+    const BookPlan bp(caps, p.T);
+    Ctl *ctl = reinterpret_cast<Ctl *>(smem + sp.ctl);
+    float *DL = reinterpret_cast<float *>(smem + sp.dl);  // [T][NM] lambda2 |g_i - dt|
+    float *fw = reinterpret_cast<float *>(smem + sp.fw);  // [FT + T][NM] frame minima of w
     float *b_ean = reinterpret_cast<float *>(smem + sp.bean);  // [NB][NM] lambda1 W^d + alpha_{i+1}(eps, b)
-    float *fw = reinterpret_cast<float *>(smem + sp.fw);       // [FT + T][NM] frame minima of w
-    float *DL = reinterpret_cast<float *>(smem + sp.dl);       // [T][NM] lambda2 |g_i - dt|
-    Seg *seg = reinterpret_cast<Seg *>(smem + sp.seg);
-    uint8_t *smap = smem + sp.map;
-    WorkItem *s_item = reinterpret_cast<WorkItem *>(smem + sp.item);            // [2] per stage
-    InstDesc *s_inst = reinterpret_cast<InstDesc *>(smem + sp.item + 2 * sizeof(WorkItem));  // [2]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + sp.item + 2 * sizeof(WorkItem) + 2 * sizeof(InstDesc));
-    uint64_t *full = bars;         // [2] item inputs landed (producer arrive + TMA bytes)
-    uint64_t *empty_in = bars + 2; // single-buffered inputs consumed (after P2)
-    uint64_t *empty_th = bars + 3; // [2] direction rows of a stage consumed (after the loop)
-    int *s_nst = reinterpret_cast<int *>(bars + 5);
-    int *s_claim = s_nst + 1;
-
     const int T = p.T;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-    for (int q = tid; q < T * NM; q += blockDim.x) {
+    for (int q = tid; q < T * NM; q += KDP_THREADS) {
         const int dt = q / NM, k = q - dt * NM;
         DL[q] = delta_term(p.l2, kc.c[k].x, dt);
     }
     if (tid == 0) {
-        mbar_init(full, 1);
-        mbar_init(full + 1, 1);
-        mbar_init(empty_in, 1);
-        mbar_init(empty_th, 1);
-        mbar_init(empty_th + 1, 1);
+        for (int st = 0; st < 2; ++st) {
+            mbar_init(&ctl->raw[st], 1);
+            mbar_init(&ctl->free_[st], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-
-    if (warp == KDP_WARPS) {  // ---------------- producer warp: claims items, streams their inputs
-        if (lane != 0) return;
-        for (int n = 0;; ++n) {
-            const int s = n & 1;
-            int idx;
-            WorkItem w{};
-            do {  // skip empty slots
-                idx = atomicAdd(counter, 1);
-                if (idx >= nitems) break;
-                w = items[idx];
-            } while (w.F1 <= w.F0);
-            InstDesc d{};
-            CopyList cl;
-            if (idx < nitems) {
-                d = inst[w.inst];
-                plan_item<NM, kHasNext>(sc, w, d, hist, L, layer, U, ui_off, T, sp, smem, s, cl);
-            } else {
-                w.inst = -1;
+    if (warp == KDP_WARPS) {  // ---------------- copy warp: item m goes to stage m % 2 once item m-2 left it
+        if (lane == 0) {
+            for (int m = 0;; ++m) {
+                const int st = m & 1;
+                if (m >= 2) mbar_wait(&ctl->free_[st], ((m - 2) >> 1) & 1);
+                const int idx = atomicAdd(counter, 1);
+                WorkItem &nw = ctl->w[st];
+                if (idx < nitems) {
+                    nw = items[idx];
+                    trace(m, 4);
+                    issue_stage<NM, kHasNext>(sc, nw, hist, L, layer, U, ui_off, T, sp, smem, st, &ctl->raw[st], book,
+                                              (unsigned)bp.total);
+                    trace(m, 5);
+                } else {
+                    nw.live = 0;
+                    mbar_arrive(&ctl->raw[st]);
+                    break;
+                }
             }
-            if (n >= 1) mbar_wait(empty_in, (n - 1) & 1);       // item n-1 finished P2
-            if (n >= 2) mbar_wait(empty_th + s, ((n - 2) >> 1) & 1);  // item n-2 finished its loop
-            s_item[s] = w;
-            s_inst[s] = d;
-            if (w.inst < 0) {
-                mbar_arrive(full + s);
-                return;
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic accesses before async writes
-            cl.issue(full + s);
         }
+        return;
     }
-
-    // ---------------- consumer warps
-    for (int n = 0;; ++n) {
-        const int stage = n & 1;
-        mbar_wait(full + stage, (n >> 1) & 1);
-        const WorkItem w = s_item[stage];
-        if (w.inst < 0) break;
-        const InstDesc d = s_inst[stage];
-        const float *TH = reinterpret_cast<const float *>(smem + (stage ? sp.th1 : sp.th0));
+    for (int m = 0;; ++m) {
+        const int s = m & 1;
+        if (tid == 0) trace(m, 0);
+        mbar_wait(&ctl->raw[s], (m >> 1) & 1);
+        if (tid == 0) trace(m, 1);
+        const WorkItem &w = ctl->w[s];
+        if (!w.live) break;
+        const InstDesc &d = w.d;
+        const float *TH = reinterpret_cast<const float *>(smem + sp.th[s]);
+        float *EN = reinterpret_cast<float *>(smem + sp.en[s]);
+        const float *UC = reinterpret_cast<const float *>(smem + sp.uc[s]);
+        const float *WE = reinterpret_cast<const float *>(smem + sp.we[s]);
+        const int *TC = reinterpret_cast<const int *>(smem + sp.tc[s]);
+        const int4 *NI = reinterpret_cast<const int4 *>(smem + sp.ni[s]);
+        const float *EB = reinterpret_cast<const float *>(smem + sp.eb[s]);
+        const float *EE = reinterpret_cast<const float *>(smem + sp.ee[s]);
+        const int *FTAB = reinterpret_cast<const int *>(smem + sp.ftab[s]);
         const int F0 = w.F0, F1 = w.F1, B0 = w.B0, B1 = w.B1, A0 = w.A0;
         const int NR = B1 - A0, NBr = B1 - B0;
         const int Sw = d.we - d.wb;
         const int wend = d.o + caps.W;
         float *cur = hist + (int64_t)layer * L + d.off;
-        const int nseg = (F1 - F0) * (T - 1);
         auto first = [&](int f) { return f <= 0 ? 0 : (f > sc.fmax ? sc.S : FTAB[w.ft0 + (f - w.flo)]); };
+        const unsigned char *bk = smem + sp.bk[s];  // the item's bookkeeping (k_item_prep)
+        const int nst = *reinterpret_cast<const int *>(bk + bp.nst);
+        const Seg *seg = reinterpret_cast<const Seg *>(bk + bp.seg);
+        const int *r_ofs = reinterpret_cast<const int *>(bk + bp.rows);  // [NA] offset of row x in TH
+        const int *r_en = r_ofs + caps.NA;  // entry index of row x's column 0 in EN
+        const int *r_q = r_en + caps.NA;    // qstart[x] (compact band: coincidence flags)
+        const int *r_qp = r_q + caps.NA;    // qpad[x] (padded band: alpha slots)
+        const int *r_fc = r_qp + caps.NA;   // first / last coincident column
+        const int *r_lc = r_fc + caps.NA;
+        const uint8_t *smap = bk + bp.map;
+        (void)NR;
 
-        // ---------------- P1: segment table + prefix (warp 0); row bookkeeping, frame minima of w (warps 1..)
-        if (warp == 0) {  // segments, gap-major: long candidate ranges first
-            int carry = 0;
-            for (int r0 = 0; r0 < nseg; r0 += 32) {
-                const int r = r0 + lane;
-                Seg sg{};
-                int cnt = 0;
-                if (r < nseg) {
-                    const int g = 1 + r / (F1 - F0);
-                    const int f = F0 + r % (F1 - F0);
-                    if (f - g >= d.o) {
-                        sg.g = g;
-                        sg.b0 = first(f);
-                        sg.nb = first(f + 1) - sg.b0;
-                        sg.a0 = first(f - g);
-                        sg.f1a = first(f - g + 1);
-                        const int c0 = first(f + 1);
-                        sg.trip = max(0, min(first(f - g + T), d.we) - c0);
-                        sg.aoff = c0 - sg.f1a;
-                        sg.inv = sg.nb > 1 ? (unsigned)((0x100000000ull + sg.nb - 1) / sg.nb) : 0u;
-                        cnt = sg.nb * (sg.f1a - sg.a0);
-                    }
-                }
-                const int incl = warp_incl_scan(cnt, lane);
-                sg.start = carry + incl - cnt;
-                if (r < nseg) seg[r] = sg;
-                carry += __shfl_sync(0xffffffffu, incl, 31);
-            }
-            if (lane == 0) {
-                *s_nst = carry;
-                *s_claim = 0;
-            }
-        } else {
-            const int t1 = tid - 32;
-            for (int r = t1; r < NR; r += KDP_THREADS - 32) {
-                const int4 ni = NI[r];  // (t', minnode(t'+1), qstart, qpad)
-                r_ofs[r] = ni.w - w.th0;  // TH[q] holds theta_pad[th0 + q]
-                r_en[r] = ni.w - w.qb0;
-                r_q[r] = ni.z;
-                r_qp[r] = ni.w;
-                r_fc[r] = RFC[w.rf0 + r];  // whole (unclipped) row: conservative
-                r_lc[r] = RLC[w.rf0 + r];
-            }
-            const int nfw = min(F1 + T - 1, wend) - F0;  // frames [F0, F1 + T - 1) inside the window
-            for (int q = t1; q < nfw * NM; q += KDP_THREADS - 32) {
-                const int fi = q / NM, k = q - fi * NM, f = F0 + fi;
-                float wm = INFINITY;
-                const int c1 = first(f + 1);
-                for (int c = first(f); c < c1; ++c)
-                    wm = fminf(wm, msg_n(kHasNext ? WE[w.we0 + (c - B0) * NM + k] : 0.f, p.l1,
-                                         UC[w.uc0 + (c - B0) * NM + k]));
-                fw[q] = wm;
-            }
+        // ---- P1: frame minima of w
+        const int nfw = min(F1 + T - 1, wend) - F0;  // frames [F0, F1 + T - 1) inside the window
+        for (int q = tid; q < nfw * NM; q += KDP_THREADS) {
+            const int fi = q / NM, k = q - fi * NM, f = F0 + fi;
+            float wm = INFINITY;
+            const int c1 = first(f + 1);
+            for (int c = first(f); c < c1; ++c)
+                wm = fminf(wm, msg_n(kHasNext ? WE[w.we0 + (c - B0) * EPF + k] : 0.f, p.l1, UC[w.uc0 + (c - B0) * NM + k]));
+            fw[q] = wm;
         }
-        consumers_sync();
+        if (tid == 0) ctl->claim[0] = 0;
+        compute_sync();
+        if (tid == 0) trace(m, 6);
 
-        // ---------------- P2: state -> segment map, messages + (b, eps), (eps, b), (eps, eps)
-        const int nst = *s_nst;
-        for (int s = warp; s < nseg; s += KDP_WARPS) {
-            const int st0 = seg[s].start, cnt = (s + 1 < nseg ? seg[s + 1].start : nst) - st0;
-            for (int q = lane; q < cnt; q += 32) smap[st0 + q] = (uint8_t)s;
-        }
+        // ---- P2: candidate entries in place + (b, eps), (eps, b), (eps, eps)
         for (int rb = warp; rb < NBr; rb += KDP_WARPS) {  // one warp per b row
             const int r = rb + (B0 - A0);
-            const int tb = NI[r].x, c0 = NI[r].y;
+            const int4 ni = NI[r];
+            const int tb = ni.x, c0 = ni.y;
             const int len = min(first(tb + T), d.we) - c0;  // candidates of row b in this window (R1, R2)
-            const int e0 = r_en[r], t0 = r_ofs[r];
+            const int e0 = ni.w - w.qb0, t0 = ni.w - w.th0;
             float mn[NM];
 #pragma unroll
             for (int k = 0; k < NM; ++k) mn[k] = INFINITY;
+#pragma unroll 2
             for (int j = lane; j < len; j += 32) {
                 const int e = e0 + j, cc = c0 + j - B0;
                 const int dt = TC[w.tc0 + cc] - tb;
                 float ent[EPF];
+                if (kHasNext) ld_entry<EPF>(EN + (size_t)e * EPF, ent);  // alpha_{i+1}(c, b), landed by TMA
+                const float *u = UC + w.uc0 + cc * NM;
+                const float *dl = DL + dt * NM;
+                // scalar on purpose: ptxas contracts a packed mul.rn.f32x2 feeding an add.rn.f32x2
+                // into FFMA2 (even with --fmad=false), which would change msg_n's rounding
 #pragma unroll
                 for (int k = 0; k < NM; ++k) {
-                    const float n = msg_n(kHasNext ? ARAW[w.araw0 + e * NM + k] : 0.f, p.l1, UC[w.uc0 + cc * NM + k]);
+                    const float n = msg_n(kHasNext ? ent[k] : 0.f, p.l1, u[k]);
                     mn[k] = fminf(mn[k], n);
-                    ent[k] = __fadd_rn(n, DL[dt * NM + k]);  // msg_m
+                    ent[k] = __fadd_rn(n, dl[k]);  // msg_m
                 }
-                ent[NM] = TH[t0 + j];
+                ent[NM] = TH[t0 + j];  // theta(b -> c)
 #pragma unroll
                 for (int k = NM + 1; k < EPF; ++k) ent[k] = 0.f;
 #pragma unroll
@@ -437,49 +431,49 @@ __global__ void __launch_bounds__(KDP_THREADS + 32, 2) k_dp_fused(SceneView sc, 
                     reinterpret_cast<float4 *>(EN + (size_t)e * EPF)[q] =
                         make_float4(ent[4 * q], ent[4 * q + 1], ent[4 * q + 2], ent[4 * q + 3]);
             }
-            float ean = 0.f, bm = INFINITY;
+            float bm = INFINITY;
 #pragma unroll
             for (int k = 0; k < NM; ++k) {  // n >= 0: float order = unsigned bit order
                 const float v = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(mn[k])));
                 if (lane == k) bm = v;
             }
             if (lane < NM) {
-                ean = __fadd_rn(p.l1W, kHasNext ? EB[w.eb0 + rb * NM + lane] : 0.f);  // lambda1 W^d + alpha_{i+1}(eps, b)
-                b_ean[rb * NM + lane] = ean;
-                cur[(int64_t)(d.ntail + B0 + rb - d.wb) * NM + lane] = fminf(bm, ean);  // (b, eps)
+                const float ean = __fadd_rn(p.l1W, kHasNext ? EB[w.eb0 + rb * EPF + lane] : 0.f);
+                b_ean[rb * NM + lane] = ean;                                             // lambda1 W^d + alpha_{i+1}(eps, b)
+                cur[(int64_t)(d.ntail + B0 + rb - d.wb) * EPF + lane] = fminf(bm, ean);  // (b, eps)
             }
         }
-        for (int q = tid; q < NBr * NM; q += KDP_THREADS) {  // (eps, b): frames (t'(b), t'(b) + T) inside the window
+        for (int q = tid; q < NBr * NM; q += KDP_THREADS) {  // (eps, b): frames (t'(b), t'(b) + T) in the window
             const int rb = q / NM, k = q - rb * NM;
             const int tb = NI[rb + (B0 - A0)].x;
             float r = INFINITY;
             const int f1 = min(tb + T, wend);
             for (int f = tb + 1; f < f1; ++f) r = fminf(r, fw[(f - F0) * NM + k]);
-            cur[(int64_t)(d.ntail + Sw + B0 + rb - d.wb) * NM + k] =
+            cur[(int64_t)(d.ntail + Sw + B0 + rb - d.wb) * EPF + k] =
                 fminf(r, __fadd_rn(p.l1W, kHasNext ? EE[w.ee0 + k] : 0.f));
         }
         if (tid < NM) {  // (eps, eps): this item's frames, min-reduced into the slot (reset to +inf by step i+1)
             float r = __fadd_rn(p.l1W, kHasNext ? EE[w.ee0 + tid] : 0.f);
             for (int f = F0; f < F1; ++f) r = fminf(r, fw[(f - F0) * NM + tid]);
-            atomicMin(reinterpret_cast<unsigned *>(cur + (int64_t)(d.ntail + 2 * Sw) * NM + tid), __float_as_uint(r));
+            atomicMin(reinterpret_cast<unsigned *>(cur + (int64_t)(d.ntail + 2 * Sw) * EPF + tid), __float_as_uint(r));
             if (has_prev && F0 == d.o)  // the next step's slot starts at +inf
-                (cur - L)[(int64_t)(d.ntail + 2 * Sw) * NM + tid] = INFINITY;
+                (cur - L)[(int64_t)(d.ntail + 2 * Sw) * EPF + tid] = INFINITY;
         }
-        consumers_sync();
-        if (tid == 0) mbar_arrive(empty_in);  // the producer may refill the single-buffered inputs
+        compute_sync();
+        if (tid == 0) trace(m, 2);
 
-        // ---------------- P4: real states (b, a)
-        for (;;) {  // warps claim 32-state groups (gap-major order: longest trips first)
+        // ---- P3: real states (b, a); warps claim 32-state groups (gap-major order: longest trips first)
+        for (;;) {
             int s0 = 0;
-            if (lane == 0) s0 = atomicAdd(s_claim, 32);
+            if (lane == 0) s0 = atomicAdd(&ctl->claim[0], 32);
             s0 = __shfl_sync(0xffffffffu, s0, 0);
             if (s0 >= nst) break;
-            const int s = s0 + lane;
-            const bool live = s < nst;
-            const Seg sg = seg[live ? smap[s] : smap[nst - 1]];
+            const int st = s0 + lane;
+            const bool live = st < nst;
+            const Seg sg = seg[live ? smap[st] : smap[nst - 1]];
             int trip = 0, b = B0, a = A0;
             if (live) {
-                const int r = s - sg.start;
+                const int r = st - sg.start;
                 const int ai = sg.nb > 1 ? (int)__umulhi((unsigned)r, sg.inv) : r;
                 b = sg.b0 + (r - ai * sg.nb);
                 a = sg.a0 + ai;
@@ -532,17 +526,22 @@ __global__ void __launch_bounds__(KDP_THREADS + 32, 2) k_dp_fused(SceneView sc, 
                 }
             }
             if (live) {
-                float out[NM];
+                float out[EPF];
 #pragma unroll
                 for (int k = 0; k < NM; ++k) {
                     const float real = __fadd_rn(R[k], state_const(p.l2, kc.c[k].y, sg.g));
                     out[k] = fminf(real, b_ean[(b - B0) * NM + k]);
                 }
-                st_alpha<NM>(cur + (int64_t)(r_qp[ra] + colb - d.ppad) * NM, out);
+#pragma unroll
+                for (int k = NM; k < EPF; ++k) out[k] = 0.f;
+                float4 *dst = reinterpret_cast<float4 *>(cur + (int64_t)(r_qp[ra] + colb - d.ppad) * EPF);
+#pragma unroll
+                for (int q = 0; q < EPF / 4; ++q) dst[q] = make_float4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]);
             }
         }
-        consumers_sync();
-        if (tid == 0) mbar_arrive(empty_th + stage);  // this stage's direction rows may be refilled
+        compute_sync();  // stage s and the item's bookkeeping are free again
+        if (tid == 0) mbar_arrive(&ctl->free_[s]);
+        if (tid == 0) trace(m, 3);
     }
 }
 
@@ -553,41 +552,116 @@ __global__ void k_init_ee(const InstDesc *__restrict__ inst, int ninst, float *_
     if (q >= ninst * NM) return;
     const int k = q / NM, m = q - k * NM;
     const InstDesc d = inst[k];
-    hist[(int64_t)layer * L + d.off + (int64_t)(d.ntail + 2 * (d.we - d.wb)) * NM + m] = INFINITY;
+    hist[(int64_t)layer * L + d.off + (int64_t)(d.ntail + 2 * (d.we - d.wb)) * entry_floats(NM) + m] = INFINITY;
 }
 
-// Work items of a chunk: slot x of window k is the x-th global tile meeting the
-// window's frames, clipped to them; descriptors are valid for every step.
+// Work items of a chunk, one thread per window: the global tiles meeting the
+// window's frames, clipped to them, at item_base[k] ...; descriptors are valid for
+// every step of the chunk.
 __global__ void k_items(SceneView sc, const InstDesc *__restrict__ inst, int ninst, int W, int T,
                         const int32_t *__restrict__ gstart, const int32_t *__restrict__ tile_of, int tf_lo,
-                        int slots, WorkItem *items) {
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= ninst * slots) return;
-    const int k = q / slots, x = q - k * slots;
+                        const int32_t *__restrict__ item_base, WorkItem *items) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= ninst) return;
     const InstDesc d = inst[k];
-    const int gt = __ldg(tile_of + (d.o - tf_lo)) + x;
-    WorkItem w{};
-    w.inst = k;
-    w.F0 = max(__ldg(gstart + gt), d.o);
-    w.F1 = min(__ldg(gstart + gt + 1), d.o + W);
-    if (w.F0 >= d.o + W) {  // no such tile: empty item (F1 <= F0)
-        w.F0 = w.F1 = d.o + W;
+    const int g0 = __ldg(tile_of + (d.o - tf_lo)), n = __ldg(item_base + k + 1) - __ldg(item_base + k);
+    for (int x = 0; x < n; ++x) {
+        WorkItem w{};
+        w.d = d;
+        w.live = 1;
+        w.idx = __ldg(item_base + k) + x;
+        w.F0 = max(__ldg(gstart + g0 + x), d.o);
+        w.F1 = min(__ldg(gstart + g0 + x + 1), d.o + W);
+        w.B0 = sc.first(w.F0);
+        w.B1 = sc.first(w.F1);
+        w.A0 = max(sc.first(w.F0 - T + 1), d.wb);
+        w.Cend = min(sc.first(w.F1 + T - 1), d.we);
+        w.qa = __ldg(sc.qpad + w.A0);
+        w.qb0 = __ldg(sc.qpad + w.B0);
+        w.qb1 = __ldg(sc.qpad + w.B1);
+        items[__ldg(item_base + k) + x] = w;
     }
-    w.B0 = sc.first(w.F0);
-    w.B1 = sc.first(w.F1);
-    w.A0 = max(sc.first(w.F0 - T + 1), d.wb);
-    w.Cend = min(sc.first(w.F1 + T - 1), d.we);
-    w.qa = __ldg(sc.qpad + w.A0);
-    w.qb0 = __ldg(sc.qpad + w.B0);
-    w.qb1 = __ldg(sc.qpad + w.B1);
-    items[q] = w;
 }
+
+// Step-independent bookkeeping of every work item of a chunk (one CTA per item):
+// the segment table of its real states (a (b-frame, a-frame) segment shares its
+// candidate range [minnode(t'(b)+1), minnode(t'(a)+T))) in
+// gap-major order with prefix starts, the state -> segment map, and the row tables.
+__global__ void __launch_bounds__(256) k_item_prep(SceneView sc, const WorkItem *__restrict__ items, TileCaps caps,
+                                                   int T, unsigned char *__restrict__ book) {
+    const BookPlan bp(caps, T);
+    const WorkItem w = items[blockIdx.x];
+    unsigned char *bk = book + (size_t)blockIdx.x * bp.total;
+    Seg *seg = reinterpret_cast<Seg *>(bk + bp.seg);
+    int *r_ofs = reinterpret_cast<int *>(bk + bp.rows);
+    int *r_en = r_ofs + caps.NA, *r_q = r_en + caps.NA, *r_qp = r_q + caps.NA, *r_fc = r_qp + caps.NA,
+        *r_lc = r_fc + caps.NA;
+    uint8_t *smap = bk + bp.map;
+    __shared__ int s_cnt[256];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int F0 = w.F0, F1 = w.F1, nseg = (F1 - F0) * (T - 1);
+    const int th0 = w.qa & ~3;  // theta_pad index the stage's TH[0] holds (the copy starts 16-byte aligned)
+    for (int r = tid; r < w.B1 - w.A0; r += blockDim.x) {
+        const int x = w.A0 + r;
+        const int4 ni = __ldg(sc.ninfo + x);  // (t', minnode(t'+1), qstart, qpad)
+        r_ofs[r] = ni.w - th0;
+        r_en[r] = ni.w - w.qb0;
+        r_q[r] = ni.z;
+        r_qp[r] = ni.w;
+        r_fc[r] = __ldg(sc.rfc + x);  // whole (unclipped) row: conservative
+        r_lc[r] = __ldg(sc.rlc + x);
+    }
+    Seg sg{};
+    int cnt = 0;
+    if (tid < nseg) {  // segments, gap-major: long candidate ranges first
+        const int g = 1 + tid / (F1 - F0);
+        const int f = F0 + tid % (F1 - F0);
+        if (f - g >= w.d.o) {
+            sg.g = g;
+            sg.b0 = sc.first(f);
+            sg.nb = sc.first(f + 1) - sg.b0;
+            sg.a0 = sc.first(f - g);
+            sg.f1a = sc.first(f - g + 1);
+            const int c0 = sc.first(f + 1);
+            sg.trip = max(0, min(sc.first(f - g + T), w.d.we) - c0);
+            sg.aoff = c0 - sg.f1a;
+            sg.inv = sg.nb > 1 ? 0xffffffffu / (unsigned)sg.nb + 1u : 0u;  // ceil(2^32 / nb)
+            cnt = sg.nb * (sg.f1a - sg.a0);
+        }
+    }
+    s_cnt[tid] = cnt;
+    __syncthreads();
+    if (warp == 0) {  // prefix over the segments (nseg <= 255)
+        int carry = 0;
+        for (int r0 = 0; r0 < nseg; r0 += 32) {
+            const int v = r0 + lane < nseg ? s_cnt[r0 + lane] : 0;
+            const int incl = warp_incl_scan(v, lane);
+            if (r0 + lane < nseg) s_cnt[r0 + lane] = carry + incl - v;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) *reinterpret_cast<int *>(bk + bp.nst) = carry;
+    }
+    __syncthreads();
+    if (tid < nseg) {
+        sg.start = s_cnt[tid];
+        seg[tid] = sg;
+        for (int q = 0; q < cnt; ++q) smap[sg.start + q] = (uint8_t)tid;
+    }
+}
+
+hgm_status launch_item_prep(const SceneView &v, const WorkItem *items, int nitems, const TileCaps &caps, int T,
+                            unsigned char *book, cudaStream_t s) {
+    if (nitems > 0) k_item_prep<<<nitems, 256, 0, s>>>(v, items, caps, T, book);
+    return HGM_OK;
+}
+
+size_t item_book_bytes(const TileCaps &caps, int T) { return BookPlan(caps, T).total; }
 
 // ------------------------------------------------------------------ launchers
 size_t dp_batch_smem(const TileCaps &c, int T, int NM) { return SmemPlan(c, T, NM).total; }
 
 template <int NM>
-static hgm_status launch_nm(const SceneView &v, const InstDesc *dinst, const WorkItem *items, int nitems,
+static hgm_status launch_nm(const SceneView &v, const WorkItem *items, int nitems, const unsigned char *book,
                             int *counter, float *hist, int64_t L, int layer, bool has_next, bool has_prev,
                             const StepConstB &kc, const float *U, int64_t ui_off, const DPParams &p,
                             const TileCaps &caps, cudaStream_t s) {
@@ -599,24 +673,46 @@ static hgm_status launch_nm(const SceneView &v, const InstDesc *dinst, const Wor
     if ((int)smem > configured[h]) {
         HGM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured[h] = (int)smem;
-        HGM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[h], kern, KDP_THREADS + 32, smem));
+        HGM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[h], kern, KDP_BLOCK, smem));
     }
     int dev = 0, nsm = 0;
     HGM_CUDA(cudaGetDevice(&dev));
     HGM_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     const int grid = std::max(1, std::min(nitems, std::max(1, blocks_per_sm[h]) * nsm));
-    kern<<<grid, KDP_THREADS + 32, smem, s>>>(v, dinst, items, nitems, counter, hist, L, layer, has_prev ? 1 : 0, kc, U,
-                                         ui_off, p, caps);
+    static int traced = 0;
+    unsigned long long *tbuf = nullptr;
+    if (getenv("HGM_TRACE") && !traced && layer == 10) {
+        traced = 1;
+        cudaMalloc(&tbuf, 64 * 8 * 8);
+        cudaMemset(tbuf, 0, 64 * 8 * 8);
+        cudaMemcpyToSymbol(g_trace, &tbuf, sizeof(tbuf));
+    }
+    kern<<<grid, KDP_BLOCK, smem, s>>>(v, items, nitems, counter, hist, L, layer, has_prev ? 1 : 0, kc, U,
+                                         ui_off, p, caps, book);
+    if (tbuf) {
+        unsigned long long h[64 * 8], *z = nullptr;
+        cudaMemcpy(h, tbuf, sizeof(h), cudaMemcpyDeviceToHost);
+        cudaMemcpyToSymbol(g_trace, &z, sizeof(z));
+        cudaFree(tbuf);
+        unsigned long long t0 = h[0];
+        fprintf(stderr, "HGM_TRACE grid=%d smem=%zu  (us since start) P:emptywait,issued,synced,raw,converted  C:wait,got,done\n",
+                grid, smem);
+        for (int m = 0; m < 64; ++m) {
+            fprintf(stderr, "%2d", m);
+            for (int e = 0; e < 8; ++e) fprintf(stderr, " %8.2f", h[m * 8 + e] ? (h[m * 8 + e] - t0) * 1e-3 : -1.0);
+            fprintf(stderr, "\n");
+        }
+    }
     return HGM_OK;
 }
 
-hgm_status launch_dp_batch(int NM, const SceneView &v, const InstDesc *dinst, const WorkItem *items, int nitems,
+hgm_status launch_dp_batch(int NM, const SceneView &v, const WorkItem *items, int nitems, const unsigned char *book,
                            int *counter, float *hist, int64_t L, int layer, bool has_next, bool has_prev,
                            const StepConstB &kc, const float *U, int64_t ui_off, const DPParams &p,
                            const TileCaps &caps, cudaStream_t s) {
 #define HGM_NM_CASE(n)                                                                                             \
     case n:                                                                                                        \
-        return launch_nm<n>(v, dinst, items, nitems, counter, hist, L, layer, has_next, has_prev, kc, U, ui_off, p, \
+        return launch_nm<n>(v, items, nitems, book, counter, hist, L, layer, has_next, has_prev, kc, U, ui_off, p, \
                             caps, s)
     switch (NM) {
         HGM_NM_CASE(1);
@@ -633,9 +729,9 @@ hgm_status launch_dp_batch(int NM, const SceneView &v, const InstDesc *dinst, co
 }
 
 hgm_status launch_items(const SceneView &v, const InstDesc *dinst, int ninst, int W, int T, const int32_t *gstart,
-                        const int32_t *tile_of, int tf_lo, int slots, WorkItem *items, cudaStream_t s) {
-    const int n = ninst * slots;
-    if (n > 0) k_items<<<(n + 255) / 256, 256, 0, s>>>(v, dinst, ninst, W, T, gstart, tile_of, tf_lo, slots, items);
+                        const int32_t *tile_of, int tf_lo, const int32_t *item_base, WorkItem *items, cudaStream_t s) {
+    if (ninst > 0)
+        k_items<<<(ninst + 127) / 128, 128, 0, s>>>(v, dinst, ninst, W, T, gstart, tile_of, tf_lo, item_base, items);
     return HGM_OK;
 }
 

@@ -70,26 +70,30 @@ struct TileCaps {  // shared-memory capacities of one K-DP work item, maxima ove
     int W;      // window length in frames
 };
 
-// One K-DP work item: a tile of b-frames [F0, F1) of window `inst` (dp_batch.cu).
+// One K-DP work item: a tile of b-frames [F0, F1) of one window (dp_batch.cu).
 struct WorkItem {
-    int inst, F0, F1;
+    InstDesc d;    // the window
+    int live;      // 0: end-of-work marker
+    int idx;       // index in the chunk's item list (its bookkeeping record)
+    int F0, F1;
     int B0, B1;    // b nodes: minnode(F0), minnode(F1)
     int A0;        // first direction row: max(minnode(F0 - T + 1), window start)
     int Cend;      // candidate nodes end: min(minnode(F1 + T - 1), window end)
     int qa, qb0, qb1;  // qpad[A0], qpad[B0], qpad[B1]
-    // filled by the prefetching thread: shared-memory index of each range's first element
-    int th0, araw0, we0, eb0, ee0, uc0, tc0, rf0, ft0, flo;
+    // filled by the producer lane: shared-memory index of each range's first element
+    int th0, we0, eb0, ee0, uc0, tc0, rf0, ft0, flo;
 };
 
 constexpr int MAX_BATCH = 8;  // models of equal M evaluated together by one CTA
 
 // Batched layouts (NM models of equal M, model index k fastest):
 //   unary    U[((i * nn) + (n - n_lo)) * NM + k]
-//   history  hist[layer * L + off + s * NM + k]   (off counts states x NM)
+//   history  hist[layer * L + off + s * SS + k]   (SS = entry_floats(NM) floats per state; v0: SS = 1)
 struct BTArgs {
     const float *U;
     int64_t nn, n_lo;
     int NM, M;
+    int SS;  // floats per state in a layer (entry_floats(NM); the model index k is slot k)
     const float4 *step[MAX_BATCH];  // per-model step constants (device)
     float *E[MAX_BATCH], *A[MAX_BATCH];
     int64_t *z[MAX_BATCH];  // [count * M] per model

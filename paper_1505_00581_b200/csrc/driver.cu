@@ -10,12 +10,15 @@
 
 namespace hgm {
 
-hgm_status launch_dp_batch(int NM, const SceneView &v, const InstDesc *dinst, const WorkItem *items, int nitems,
+hgm_status launch_item_prep(const SceneView &v, const WorkItem *items, int nitems, const TileCaps &caps, int T,
+                            unsigned char *book, cudaStream_t s);
+size_t item_book_bytes(const TileCaps &caps, int T);
+hgm_status launch_dp_batch(int NM, const SceneView &v, const WorkItem *items, int nitems, const unsigned char *book,
                            int *counter, float *hist, int64_t L, int layer, bool has_next, bool has_prev,
                            const StepConstB &kc, const float *U, int64_t ui_off, const DPParams &p,
                            const TileCaps &caps, cudaStream_t s);
 hgm_status launch_items(const SceneView &v, const InstDesc *dinst, int ninst, int W, int T, const int32_t *gstart,
-                        const int32_t *tile_of, int tf_lo, int slots, WorkItem *items, cudaStream_t s);
+                        const int32_t *tile_of, int tf_lo, const int32_t *item_base, WorkItem *items, cudaStream_t s);
 hgm_status launch_init_ee(const InstDesc *dinst, int ninst, float *hist, int64_t L, int layer, int NM,
                           cudaStream_t s);
 size_t dp_batch_smem(const TileCaps &c, int T, int NM);
@@ -70,7 +73,7 @@ static bool make_tiling(const hgm_scene *sc, const hgm_offsets &o, int T, int NM
     const int FT_max = std::max(1, std::min(8, 255 / std::max(1, T - 1)));
     const char *benv = getenv("HGM_SMEM_KB");  // tuning knob: shared memory per CTA (2 CTAs per SM by default)
     const size_t budgets[2] = {(size_t)(benv ? atoi(benv) : 110) * 1024, 220 * 1024};
-    const int64_t ent_bytes = 4 * (entry_floats(NM) + NM);  // EN + raw alpha per candidate entry
+    const int64_t ent_bytes = 4 * 2 * entry_floats(NM);  // 2 stages of candidate entries
     for (int bi = 0; bi < 2; ++bi)
     for (int64_t cap = (int64_t)budgets[bi]; cap >= 4096; cap = cap * 7 / 8) {
         const size_t budget = budgets[bi];
@@ -174,6 +177,8 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
     bt.n_lo = n_lo;
     bt.NM = NM;
     bt.M = M;
+    const int SS = v0 ? 1 : entry_floats(NM);  // floats per state in a layer (16-byte aligned for K-DP's copies)
+    bt.SS = SS;
     for (int k = 0; k < NM; ++k) {
         bt.step[k] = models[k]->step;
         bt.E[k] = outs[k].E;
@@ -186,8 +191,9 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
     const int nlanes = (senv && atoi(senv) == 2) ? 2 : 1;
     struct Lane {
         cudaStream_t s = nullptr;
-        DevBuf hist, dinst, items, counters;
-        int64_t hist_cap = 0, dinst_cap = 0, items_cap = 0, counters_cap = 0;
+        DevBuf hist, dinst, items, counters, ibase, book;
+        int64_t hist_cap = 0, dinst_cap = 0, items_cap = 0, counters_cap = 0, ibase_cap = 0, book_cap = 0;
+        std::vector<int32_t> ibase_h;
     } lanes[2];
     lanes[0].s = s;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -208,9 +214,9 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
         while (k1 < count && k1 - k0 < chunk_max) {
             InstDesc &d = all[k1];
             const int64_t ns = (int64_t)d.ntail + 2 * (int64_t)(d.we - d.wb) + 1;
-            if (k1 > k0 && (L + ns * NM) * std::max(nsteps, 1) > budget_floats) break;
+            if (k1 > k0 && (L + ns * SS) * std::max(nsteps, 1) > budget_floats) break;
             d.off = L;
-            L += ns * NM;
+            L += ns * SS;
             maxNs = std::max(maxNs, ns);
             ++k1;
         }
@@ -232,8 +238,22 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
         }
         const InstDesc *di = ln.dinst.as<InstDesc>();
         float *hist = ln.hist.as<float>();
-        const int nitems = ninst * tl.slots;
+        int nitems = 0;
         if (!v0 && nsteps > 0) {
+            // work items of each window: the tiles meeting its frames (host prefix, device fill)
+            ln.ibase_h.resize(ninst + 1);
+            ln.ibase_h[0] = 0;
+            for (int k = 0; k < ninst; ++k) {
+                const int of = all[k0 + k].o;
+                ln.ibase_h[k + 1] = ln.ibase_h[k] + tl.tile_of[of + o.window - 1 - tl.f_lo] - tl.tile_of[of - tl.f_lo] + 1;
+            }
+            nitems = ln.ibase_h[ninst];
+            if (ninst + 1 > ln.ibase_cap) {
+                if ((st = ln.ibase.alloc(sizeof(int32_t) * (ninst + 1), ls)) != HGM_OK) break;
+                ln.ibase_cap = ninst + 1;
+            }
+            HGM_CUDA(cudaMemcpyAsync(ln.ibase.p, ln.ibase_h.data(), sizeof(int32_t) * (ninst + 1), cudaMemcpyHostToDevice,
+                                     ls));
             if (nitems > ln.items_cap) {
                 if ((st = ln.items.alloc(sizeof(WorkItem) * nitems, ls)) != HGM_OK) break;
                 ln.items_cap = nitems;
@@ -244,9 +264,15 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
             }
             HGM_CUDA(cudaMemsetAsync(ln.counters.p, 0, sizeof(int) * nsteps, ls));
             launch_items(v, di, ninst, o.window, p.T, d_gstart.as<int32_t>(), d_tile_of.as<int32_t>(), tl.f_lo,
-                         tl.slots, ln.items.as<WorkItem>(), ls);
+                         ln.ibase.as<int32_t>(), ln.items.as<WorkItem>(), ls);
+            const int64_t bbytes = (int64_t)item_book_bytes(tl.caps, p.T) * nitems + 16;
+            if (bbytes > ln.book_cap) {
+                if ((st = ln.book.alloc(bbytes, ls)) != HGM_OK) break;
+                ln.book_cap = bbytes;
+            }
+            launch_item_prep(v, ln.items.as<WorkItem>(), nitems, tl.caps, p.T, ln.book.as<unsigned char>(), ls);
             launch_init_ee(di, ninst, hist, L, nsteps - 1, NM, ls);  // first layer's (eps, eps) slots
-            count_launch(K_DP, 2);
+            count_launch(K_DP, 3);
         }
         for (int i = M - 1; i >= 2 && st == HGM_OK; --i) {
             const bool has_next = i + 1 <= M - 1;
@@ -267,7 +293,7 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
             }
             {
                 Timer tm(ls, K_DP);
-                st = launch_dp_batch(NM, v, di, ln.items.as<WorkItem>(), nitems, ln.counters.as<int>() + (i - 2), hist,
+                st = launch_dp_batch(NM, v, ln.items.as<WorkItem>(), nitems, ln.book.as<unsigned char>(), ln.counters.as<int>() + (i - 2), hist,
                                      L, i - 2, has_next, /*has_prev=*/i - 1 >= 2, kc, U,
                                      ((int64_t)i * nn - n_lo) * NM, p, tl.caps, ls);
                 count_launch(K_DP);
