@@ -83,14 +83,46 @@ struct BookPlan {
     }
 };
 
-// Shared memory: two STAGES, each the TMA target of one work item (its candidate
-// entries -- the alpha_{i+1} rows land there in the layer's own layout and become
-// messages in place --, its direction rows and its small raw inputs), plus the
-// bookkeeping of the item being processed (rows, segments, state map, dummy terms).
-// While one item is processed the copies of the next one land in the other stage.
+// One STAGE holds everything of one work item, laid out for that item's sizes: its
+// candidate entries (the alpha_{i+1} rows land there by TMA in the layer's own layout
+// and become messages in place), its direction rows, the small raw inputs, its
+// bookkeeping record and the dummy terms of its b rows.  Byte offsets within the stage:
+struct StageLayout {
+    int en, th, uc, we, tc, ni, eb, ee, ftab, bk, bean, total;
+    StageLayout() = default;
+    // NE entries, NTH direction floats, NC candidate nodes, NA rows, NB b nodes, FT b-frames
+    __host__ __device__ StageLayout(int NE, int NTH, int NC, int NA, int NB, int FT, int T, int NM, int book) {
+        const int EPF = entry_floats(NM);
+        int o = 0;
+        auto take = [&](long long bytes) {
+            const int r = o;
+            o = (int)align16((size_t)(o + bytes));
+            return r;
+        };
+        en = take(4LL * EPF * NE);
+        th = take(4LL * (NTH + 8));  // + 8: the copies widen ranges to whole 16-byte units
+        uc = take(4LL * (NM * NC + 8));
+        we = take(4LL * (EPF * NC + 8));
+        tc = take(4LL * (NC + 8));
+        ni = take(16LL * (NA + 1));
+        eb = take(4LL * (EPF * NB + 8));
+        ee = take(4LL * (EPF + 8));
+        ftab = take(4LL * (FT + 2 * T + 16));
+        bk = take(book);
+        bean = take(4LL * NM * NB);
+        total = o;
+    }
+};
+
+__host__ __device__ inline StageLayout item_layout(const WorkItem &w, int T, int NM, int book) {
+    return StageLayout(w.qb1 - w.qb0, w.qb1 - w.qa, w.Cend - w.B0, w.B1 - w.A0, w.B1 - w.B0, w.F1 - w.F0, T, NM, book);
+}
+
+// Shared memory: two stages of caps.STAGE bytes (the largest item layout of the call;
+// while one item is processed the copies of the next one land in the other stage),
+// the copy warp's frame minima, the Delta table and the control block.
 struct SmemPlan {
-    size_t en[2], th[2], uc[2], we[2], tc[2], ni[2], eb[2], ee[2], ftab[2], bk[2];
-    size_t bean, fw, dl, ctl, total;
+    size_t stage[2], fw, dl, ctl, total;
     __host__ __device__ SmemPlan(const TileCaps &c, int T, int NM) {
         size_t o = 0;
         auto take = [&](size_t bytes) {
@@ -98,23 +130,11 @@ struct SmemPlan {
             o = align16(o + bytes);
             return r;
         };
-        const int EPF = entry_floats(NM);
-        for (int s = 0; s < 2; ++s) {
-            en[s] = take(sizeof(float) * (size_t)EPF * c.NE);
-            th[s] = take(sizeof(float) * ((size_t)c.TH + 8));
-            uc[s] = take(sizeof(float) * ((size_t)NM * c.NC + 8));
-            we[s] = take(sizeof(float) * ((size_t)EPF * c.NC + 8));
-            tc[s] = take(sizeof(int) * ((size_t)c.NC + 8));
-            ni[s] = take(sizeof(int4) * ((size_t)c.NA + 1));
-            bk[s] = take(BookPlan(c, T).total);
-            eb[s] = take(sizeof(float) * ((size_t)EPF * c.NB + 8));
-            ee[s] = take(sizeof(float) * ((size_t)EPF + 8));
-            ftab[s] = take(sizeof(int) * ((size_t)c.FT + 2 * T + 16));
-        }
-        bean = take(sizeof(float) * (size_t)NM * c.NB);
+        stage[0] = take((size_t)c.STAGE);
+        stage[1] = take((size_t)c.STAGE);
         fw = take(sizeof(float) * (size_t)NM * (c.FT + T));
         dl = take(sizeof(float) * (size_t)NM * T);
-        ctl = take(512);  // item descriptors, mbarriers, counters
+        ctl = take(1024);  // item descriptors and layouts, mbarriers, counters
         total = o;
     }
 };
@@ -253,14 +273,17 @@ __device__ __forceinline__ void trace(int m, int ev) {
 // Control block in shared memory.
 struct Ctl {
     WorkItem w[2];      // stage descriptors (w[s].live == 0: no more items)
-    int nst[2];         // real states of the current item
-    int claim[2];       // next unclaimed 32-state group
+    StageLayout lay[2]; // stage layouts
+    int row_claim[2];   // next unconverted b row of the stage's item
+    int task_claim[2];  // next unclaimed 32-task group
     uint64_t raw[2];    // stage inputs landed (copy-warp arrival + TMA bytes)
-    uint64_t free_[2];  // stage released by the compute warps
+    uint64_t conv[2];   // every b row converted (one tx unit per row)
+    uint64_t free_[2];  // stage released: one arrival per compute warp
 };
 
-// barrier of the compute warps only (the copy warp never joins it)
-__device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 1, %0;" ::"n"(KDP_THREADS) : "memory"); }
+__device__ __forceinline__ void mbar_complete_tx(uint64_t *bar, unsigned n) {
+    asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(n) : "memory");
+}
 
 // Issue the input copies of item (w, d) into stage s (producer lane 0): the alpha_{i+1}
 // rows of the tile's b nodes straight into the candidate-entry area (the layer's state
@@ -273,25 +296,27 @@ __device__ __forceinline__ void issue_stage(const SceneView &sc, WorkItem &w, co
                                             const unsigned char *__restrict__ book, unsigned book_bytes) {
     constexpr int EPF = entry_floats(NM);
     const InstDesc &d = w.d;
+    const StageLayout ly = item_layout(w, T, NM, (int)book_bytes);
+    unsigned char *sb = smem + sp.stage[s];
     Copier cl(bar);
     const int64_t nxo = (int64_t)(layer + 1) * L + d.off;  // alpha layer i+1 of this window (from the aligned base)
     const int Sw = d.we - d.wb;
     if (kHasNext) {
-        cl.range(smem + sp.en[s], hist, nxo + (int64_t)(w.qb0 - d.ppad) * EPF, nxo + (int64_t)(w.qb1 - d.ppad) * EPF);
-        w.we0 = cl.range(smem + sp.we[s], hist, nxo + (int64_t)(d.ntail + w.B0 - d.wb) * EPF,
+        cl.range(sb + ly.en, hist, nxo + (int64_t)(w.qb0 - d.ppad) * EPF, nxo + (int64_t)(w.qb1 - d.ppad) * EPF);
+        w.we0 = cl.range(sb + ly.we, hist, nxo + (int64_t)(d.ntail + w.B0 - d.wb) * EPF,
                          nxo + (int64_t)(d.ntail + w.Cend - d.wb) * EPF);
-        w.eb0 = cl.range(smem + sp.eb[s], hist, nxo + (int64_t)(d.ntail + Sw + w.B0 - d.wb) * EPF,
+        w.eb0 = cl.range(sb + ly.eb, hist, nxo + (int64_t)(d.ntail + Sw + w.B0 - d.wb) * EPF,
                          nxo + (int64_t)(d.ntail + Sw + w.B1 - d.wb) * EPF);
-        w.ee0 = cl.range(smem + sp.ee[s], hist, nxo + (int64_t)(d.ntail + 2 * Sw) * EPF,
+        w.ee0 = cl.range(sb + ly.ee, hist, nxo + (int64_t)(d.ntail + 2 * Sw) * EPF,
                          nxo + (int64_t)(d.ntail + 2 * Sw + 1) * EPF);
     }
-    w.th0 = w.qa - cl.range(smem + sp.th[s], sc.theta_pad, w.qa, w.qb1);  // TH[q] holds theta_pad[th0 + q]
-    w.uc0 = cl.range(smem + sp.uc[s], U, ui_off + (int64_t)w.B0 * NM, ui_off + (int64_t)w.Cend * NM);
-    w.tc0 = cl.range(smem + sp.tc[s], sc.t, w.B0, w.Cend);
-    if (w.B1 > w.A0) cl.raw(smem + sp.ni[s], sc.ninfo + w.A0, (unsigned)(sizeof(int4) * (w.B1 - w.A0)));
-    cl.raw(smem + sp.bk[s], book + (size_t)w.idx * book_bytes, book_bytes);  // the item's bookkeeping
+    w.th0 = w.qa - cl.range(sb + ly.th, sc.theta_pad, w.qa, w.qb1);  // TH[q] holds theta_pad[th0 + q]
+    w.uc0 = cl.range(sb + ly.uc, U, ui_off + (int64_t)w.B0 * NM, ui_off + (int64_t)w.Cend * NM);
+    w.tc0 = cl.range(sb + ly.tc, sc.t, w.B0, w.Cend);
+    if (w.B1 > w.A0) cl.raw(sb + ly.ni, sc.ninfo + w.A0, (unsigned)(sizeof(int4) * (w.B1 - w.A0)));
+    cl.raw(sb + ly.bk, book + (size_t)w.idx * book_bytes, book_bytes);  // the item's bookkeeping
     const int f_lo = max(0, w.F0 - T), f_hi = min(sc.fmax + 1, w.F1 + T);  // first_tab over [F0 - T, F1 + T]
-    w.ft0 = cl.range(smem + sp.ftab[s], sc.ft, f_lo, f_hi + 1);
+    w.ft0 = cl.range(sb + ly.ftab, sc.ft, f_lo, f_hi + 1);
     w.flo = f_lo;
     cl.close();  // (the stage was released by the consumers' empty[s] arrivals, after their reads)
 }
@@ -310,7 +335,6 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
     Ctl *ctl = reinterpret_cast<Ctl *>(smem + sp.ctl);
     float *DL = reinterpret_cast<float *>(smem + sp.dl);  // [T][NM] lambda2 |g_i - dt|
     float *fw = reinterpret_cast<float *>(smem + sp.fw);  // [FT + T][NM] frame minima of w
-    float *b_ean = reinterpret_cast<float *>(smem + sp.bean);  // [NB][NM] lambda1 W^d + alpha_{i+1}(eps, b)
     const int T = p.T;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
@@ -321,30 +345,79 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
     if (tid == 0) {
         for (int st = 0; st < 2; ++st) {
             mbar_init(&ctl->raw[st], 1);
-            mbar_init(&ctl->free_[st], 1);
+            mbar_init(&ctl->conv[st], 1);
+            mbar_init(&ctl->free_[st], KDP_WARPS);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (warp == KDP_WARPS) {  // ---------------- copy warp: item m goes to stage m % 2 once item m-2 left it
-        if (lane == 0) {
-            for (int m = 0;; ++m) {
-                const int st = m & 1;
-                if (m >= 2) mbar_wait(&ctl->free_[st], ((m - 2) >> 1) & 1);
+    if (warp == KDP_WARPS) {
+        // ---------------- copy warp: item m goes to stage m % 2 once item m-2 left it; it
+        // also computes the dummy-form states (eps, b) and (eps, eps) of each item
+        for (int m = 0;; ++m) {
+            const int st = m & 1;
+            if (m >= 2) mbar_wait(&ctl->free_[st], ((m - 2) >> 1) & 1);
+            if (lane == 0) {
                 const int idx = atomicAdd(counter, 1);
                 WorkItem &nw = ctl->w[st];
                 if (idx < nitems) {
                     nw = items[idx];
-                    trace(m, 4);
+                    ctl->lay[st] = item_layout(nw, T, NM, (int)bp.total);
+                    ctl->row_claim[st] = 0;
+                    ctl->task_claim[st] = 0;
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&ctl->conv[st])),
+                                 "r"((unsigned)(nw.B1 - nw.B0))
+                                 : "memory");
                     issue_stage<NM, kHasNext>(sc, nw, hist, L, layer, U, ui_off, T, sp, smem, st, &ctl->raw[st], book,
                                               (unsigned)bp.total);
-                    trace(m, 5);
                 } else {
                     nw.live = 0;
                     mbar_arrive(&ctl->raw[st]);
-                    break;
                 }
             }
+            mbar_wait(&ctl->raw[st], (m >> 1) & 1);
+            const WorkItem &w = ctl->w[st];
+            if (!w.live) break;
+            const InstDesc &d = w.d;
+            const StageLayout &ly = ctl->lay[st];
+            const unsigned char *sb = smem + sp.stage[st];
+            const float *UC = reinterpret_cast<const float *>(sb + ly.uc);
+            const float *WE = reinterpret_cast<const float *>(sb + ly.we);
+            const int4 *NI = reinterpret_cast<const int4 *>(sb + ly.ni);
+            const float *EE = reinterpret_cast<const float *>(sb + ly.ee);
+            const int *FTAB = reinterpret_cast<const int *>(sb + ly.ftab);
+            auto first = [&](int f) { return f <= 0 ? 0 : (f > sc.fmax ? sc.S : FTAB[w.ft0 + (f - w.flo)]); };
+            const int F0 = w.F0, F1 = w.F1, B0 = w.B0, NBr = w.B1 - w.B0, Sw = d.we - d.wb;
+            const int wend = d.o + caps.W;
+            float *cur = hist + (int64_t)layer * L + d.off;
+            const int nfw = min(F1 + T - 1, wend) - F0;  // frames [F0, F1 + T - 1) inside the window
+            for (int q = lane; q < nfw * NM; q += 32) {  // frame minima of w(c) = alpha_{i+1}(c, eps) + lambda1 U_i(c)
+                const int fi = q / NM, k = q - fi * NM, f = F0 + fi;
+                float wm = INFINITY;
+                const int c1 = first(f + 1);
+                for (int c = first(f); c < c1; ++c)
+                    wm = fminf(wm, msg_n(kHasNext ? WE[w.we0 + (c - B0) * EPF + k] : 0.f, p.l1,
+                                         UC[w.uc0 + (c - B0) * NM + k]));
+                fw[q] = wm;
+            }
+            __syncwarp();
+            for (int q = lane; q < NBr * NM; q += 32) {  // (eps, b): frames (t'(b), t'(b) + T) in the window
+                const int rb = q / NM, k = q - rb * NM;
+                const int tb = NI[rb + (B0 - w.A0)].x;
+                float r = INFINITY;
+                const int f1 = min(tb + T, wend);
+                for (int f = tb + 1; f < f1; ++f) r = fminf(r, fw[(f - F0) * NM + k]);
+                cur[(int64_t)(d.ntail + Sw + B0 + rb - d.wb) * EPF + k] =
+                    fminf(r, __fadd_rn(p.l1W, kHasNext ? EE[w.ee0 + k] : 0.f));
+            }
+            if (lane < NM) {  // (eps, eps): this item's frames, min-reduced into the slot (reset to +inf by step i+1)
+                float r = __fadd_rn(p.l1W, kHasNext ? EE[w.ee0 + lane] : 0.f);
+                for (int f = F0; f < F1; ++f) r = fminf(r, fw[(f - F0) * NM + lane]);
+                atomicMin(reinterpret_cast<unsigned *>(cur + (int64_t)(d.ntail + 2 * Sw) * EPF + lane), __float_as_uint(r));
+                if (has_prev && F0 == d.o)  // the next step's slot starts at +inf
+                    (cur - L)[(int64_t)(d.ntail + 2 * Sw) * EPF + lane] = INFINITY;
+            }
+            __syncwarp();
         }
         return;
     }
@@ -356,22 +429,23 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
         const WorkItem &w = ctl->w[s];
         if (!w.live) break;
         const InstDesc &d = w.d;
-        const float *TH = reinterpret_cast<const float *>(smem + sp.th[s]);
-        float *EN = reinterpret_cast<float *>(smem + sp.en[s]);
-        const float *UC = reinterpret_cast<const float *>(smem + sp.uc[s]);
-        const float *WE = reinterpret_cast<const float *>(smem + sp.we[s]);
-        const int *TC = reinterpret_cast<const int *>(smem + sp.tc[s]);
-        const int4 *NI = reinterpret_cast<const int4 *>(smem + sp.ni[s]);
-        const float *EB = reinterpret_cast<const float *>(smem + sp.eb[s]);
-        const float *EE = reinterpret_cast<const float *>(smem + sp.ee[s]);
-        const int *FTAB = reinterpret_cast<const int *>(smem + sp.ftab[s]);
+        const StageLayout &ly = ctl->lay[s];
+        unsigned char *sb = smem + sp.stage[s];
+        float *b_ean = reinterpret_cast<float *>(sb + ly.bean);  // [NB][NM] lambda1 W^d + alpha_{i+1}(eps, b)
+        const float *TH = reinterpret_cast<const float *>(sb + ly.th);
+        float *EN = reinterpret_cast<float *>(sb + ly.en);
+        const float *UC = reinterpret_cast<const float *>(sb + ly.uc);
+        const int *TC = reinterpret_cast<const int *>(sb + ly.tc);
+        const int4 *NI = reinterpret_cast<const int4 *>(sb + ly.ni);
+        const float *EB = reinterpret_cast<const float *>(sb + ly.eb);
+        const int *FTAB = reinterpret_cast<const int *>(sb + ly.ftab);
         const int F0 = w.F0, F1 = w.F1, B0 = w.B0, B1 = w.B1, A0 = w.A0;
         const int NR = B1 - A0, NBr = B1 - B0;
         const int Sw = d.we - d.wb;
         const int wend = d.o + caps.W;
         float *cur = hist + (int64_t)layer * L + d.off;
         auto first = [&](int f) { return f <= 0 ? 0 : (f > sc.fmax ? sc.S : FTAB[w.ft0 + (f - w.flo)]); };
-        const unsigned char *bk = smem + sp.bk[s];  // the item's bookkeeping (k_item_prep)
+        const unsigned char *bk = sb + ly.bk;  // the item's bookkeeping (k_item_prep)
         const int nst = *reinterpret_cast<const int *>(bk + bp.nst);
         const Seg *seg = reinterpret_cast<const Seg *>(bk + bp.seg);
         const int *r_ofs = reinterpret_cast<const int *>(bk + bp.rows);  // [NA] offset of row x in TH
@@ -383,22 +457,13 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
         const uint8_t *smap = bk + bp.map;
         (void)NR;
 
-        // ---- P1: frame minima of w
-        const int nfw = min(F1 + T - 1, wend) - F0;  // frames [F0, F1 + T - 1) inside the window
-        for (int q = tid; q < nfw * NM; q += KDP_THREADS) {
-            const int fi = q / NM, k = q - fi * NM, f = F0 + fi;
-            float wm = INFINITY;
-            const int c1 = first(f + 1);
-            for (int c = first(f); c < c1; ++c)
-                wm = fminf(wm, msg_n(kHasNext ? WE[w.we0 + (c - B0) * EPF + k] : 0.f, p.l1, UC[w.uc0 + (c - B0) * NM + k]));
-            fw[q] = wm;
-        }
-        if (tid == 0) ctl->claim[0] = 0;
-        compute_sync();
-        if (tid == 0) trace(m, 6);
-
-        // ---- P2: candidate entries in place + (b, eps), (eps, b), (eps, eps)
-        for (int rb = warp; rb < NBr; rb += KDP_WARPS) {  // one warp per b row
+        // ---- messages: warps claim b rows; each row's entries become messages in place and
+        // its (b, eps) state is finished; every finished row completes one tx unit of conv[s]
+        for (;;) {
+            int rb = 0;
+            if (lane == 0) rb = atomicAdd(&ctl->row_claim[s], 1);
+            rb = __shfl_sync(0xffffffffu, rb, 0);
+            if (rb >= NBr) break;
             const int r = rb + (B0 - A0);
             const int4 ni = NI[r];
             const int tb = ni.x, c0 = ni.y;
@@ -442,105 +507,123 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
                 b_ean[rb * NM + lane] = ean;                                             // lambda1 W^d + alpha_{i+1}(eps, b)
                 cur[(int64_t)(d.ntail + B0 + rb - d.wb) * EPF + lane] = fminf(bm, ean);  // (b, eps)
             }
+            __syncwarp();
+            if (lane == 0) mbar_complete_tx(&ctl->conv[s], 1);
         }
-        for (int q = tid; q < NBr * NM; q += KDP_THREADS) {  // (eps, b): frames (t'(b), t'(b) + T) in the window
-            const int rb = q / NM, k = q - rb * NM;
-            const int tb = NI[rb + (B0 - A0)].x;
-            float r = INFINITY;
-            const int f1 = min(tb + T, wend);
-            for (int f = tb + 1; f < f1; ++f) r = fminf(r, fw[(f - F0) * NM + k]);
-            cur[(int64_t)(d.ntail + Sw + B0 + rb - d.wb) * EPF + k] =
-                fminf(r, __fadd_rn(p.l1W, kHasNext ? EE[w.ee0 + k] : 0.f));
-        }
-        if (tid < NM) {  // (eps, eps): this item's frames, min-reduced into the slot (reset to +inf by step i+1)
-            float r = __fadd_rn(p.l1W, kHasNext ? EE[w.ee0 + tid] : 0.f);
-            for (int f = F0; f < F1; ++f) r = fminf(r, fw[(f - F0) * NM + tid]);
-            atomicMin(reinterpret_cast<unsigned *>(cur + (int64_t)(d.ntail + 2 * Sw) * EPF + tid), __float_as_uint(r));
-            if (has_prev && F0 == d.o)  // the next step's slot starts at +inf
-                (cur - L)[(int64_t)(d.ntail + 2 * Sw) * EPF + tid] = INFINITY;
-        }
-        compute_sync();
-        if (tid == 0) trace(m, 2);
-
-        // ---- P3: real states (b, a); warps claim 32-state groups (gap-major order: longest trips first)
+        mbar_wait(&ctl->conv[s], (m >> 1) & 1);  // all rows of the item are messages now
+        // ---- P3: real states.  A lane task is one b with a PAIR of a's of the same a-frame
+        // (same candidate range), so each candidate entry (b, c_j) is loaded once for two
+        // states; warps claim 32-task groups (gap-major order: longest trips first).
         for (;;) {
             int s0 = 0;
-            if (lane == 0) s0 = atomicAdd(&ctl->claim[0], 32);
+            if (lane == 0) s0 = atomicAdd(&ctl->task_claim[s], 32);
             s0 = __shfl_sync(0xffffffffu, s0, 0);
             if (s0 >= nst) break;
             const int st = s0 + lane;
             const bool live = st < nst;
             const Seg sg = seg[live ? smap[st] : smap[nst - 1]];
-            int trip = 0, b = B0, a = A0;
+            int trip = 0, b = B0, a0 = A0;
+            bool two = false;
             if (live) {
                 const int r = st - sg.start;
-                const int ai = sg.nb > 1 ? (int)__umulhi((unsigned)r, sg.inv) : r;
-                b = sg.b0 + (r - ai * sg.nb);
-                a = sg.a0 + ai;
+                const int ci = sg.nb > 1 ? (int)__umulhi((unsigned)r, sg.inv) : r;
+                b = sg.b0 + (r - ci * sg.nb);
+                a0 = sg.a0 + 2 * ci;
+                two = a0 + 1 < sg.f1a;
                 trip = sg.trip;
             }
-            const int ra = a - A0, rbt = b - A0;
-            const int colb = b - sg.f1a;  // column of b in row a
+            const int a1 = two ? a0 + 1 : a0;
+            const int ra0 = a0 - A0, ra1 = a1 - A0, rbt = b - A0;
+            const int colb = b - sg.f1a;  // column of b in the rows of the a-frame
             const float *erow = EN + (size_t)r_en[rbt] * EPF;
-            const float *arow = TH + r_ofs[ra] + sg.aoff;
-            const float th_ab = live ? TH[r_ofs[ra] + colb] : 0.f;
-            const int lca = r_lc[ra];
-            const bool dirty = live && ((lca >= 0 && lca >= min(colb, sg.aoff) &&
-                                         r_fc[ra] <= max(colb, sg.aoff + trip - 1)) || r_fc[rbt] < trip);
-            float R[NM];
+            const float *arow0 = TH + r_ofs[ra0] + sg.aoff, *arow1 = TH + r_ofs[ra1] + sg.aoff;
+            const float th_ab0 = live ? TH[r_ofs[ra0] + colb] : 0.f, th_ab1 = live ? TH[r_ofs[ra1] + colb] : 0.f;
+            auto dirty_of = [&](int ra) {
+                const int lca = r_lc[ra];
+                return (lca >= 0 && lca >= min(colb, sg.aoff) && r_fc[ra] <= max(colb, sg.aoff + trip - 1));
+            };
+            const bool dirty = live && (dirty_of(ra0) || dirty_of(ra1) || r_fc[rbt] < trip);
+            float R0[NM], R1[NM];
 #pragma unroll
-            for (int k = 0; k < NM; ++k) R[k] = INFINITY;
+            for (int k = 0; k < NM; ++k) R0[k] = R1[k] = INFINITY;
             if (!__any_sync(0xffffffffu, dirty)) {
                 int j = 0;
                 for (; j + 1 < trip; j += 2) {
                     float e0[EPF], e1[EPF];
                     ld_entry<EPF>(erow + (size_t)j * EPF, e0);
                     ld_entry<EPF>(erow + (size_t)(j + 1) * EPF, e1);
-                    const float ac0 = arow[j], ac1 = arow[j + 1];
-                    float v0[NM], v1[NM];
-                    cand_values<NM>(fold(e0[NM], th_ab), fold(e0[NM], ac0), e0, kc, p.l23, v0);
-                    cand_values<NM>(fold(e1[NM], th_ab), fold(e1[NM], ac1), e1, kc, p.l23, v1);
+                    {
+                        float v0[NM], v1[NM];
+                        cand_values<NM>(fold(e0[NM], th_ab0), fold(e0[NM], arow0[j]), e0, kc, p.l23, v0);
+                        cand_values<NM>(fold(e1[NM], th_ab0), fold(e1[NM], arow0[j + 1]), e1, kc, p.l23, v1);
 #pragma unroll
-                    for (int k = 0; k < NM; ++k) R[k] = min3(R[k], v0[k], v1[k]);
+                        for (int k = 0; k < NM; ++k) R0[k] = min3(R0[k], v0[k], v1[k]);
+                    }
+                    {
+                        float v0[NM], v1[NM];
+                        cand_values<NM>(fold(e0[NM], th_ab1), fold(e0[NM], arow1[j]), e0, kc, p.l23, v0);
+                        cand_values<NM>(fold(e1[NM], th_ab1), fold(e1[NM], arow1[j + 1]), e1, kc, p.l23, v1);
+#pragma unroll
+                        for (int k = 0; k < NM; ++k) R1[k] = min3(R1[k], v0[k], v1[k]);
+                    }
                 }
                 if (j < trip) {
                     float e0[EPF];
                     ld_entry<EPF>(erow + (size_t)j * EPF, e0);
-                    float v0[NM];
-                    cand_values<NM>(fold(e0[NM], th_ab), fold(e0[NM], arow[j]), e0, kc, p.l23, v0);
+                    float v0[NM], v1[NM];
+                    cand_values<NM>(fold(e0[NM], th_ab0), fold(e0[NM], arow0[j]), e0, kc, p.l23, v0);
+                    cand_values<NM>(fold(e0[NM], th_ab1), fold(e0[NM], arow1[j]), e0, kc, p.l23, v1);
 #pragma unroll
-                    for (int k = 0; k < NM; ++k) R[k] = fminf(R[k], v0[k]);
+                    for (int k = 0; k < NM; ++k) {
+                        R0[k] = fminf(R0[k], v0[k]);
+                        R1[k] = fminf(R1[k], v1[k]);
+                    }
                 }
-            } else {
-                const int qa = r_q[ra], qb = r_q[rbt];
-                const bool co_ab = live && __ldg(sc.coinc + qa + colb);
+            } else {  // exact flag-aware loop (coincident points, R10)
+                const int qb = r_q[rbt];
+                const int qa0 = r_q[ra0], qa1 = r_q[ra1];
+                const bool co_ab0 = live && __ldg(sc.coinc + qa0 + colb);
+                const bool co_ab1 = live && __ldg(sc.coinc + qa1 + colb);
                 for (int j = 0; j < trip; ++j) {
                     float e0[EPF];
                     ld_entry<EPF>(erow + (size_t)j * EPF, e0);
                     const bool cbc = __ldg(sc.coinc + qb + j);
-                    const bool cac = __ldg(sc.coinc + qa + sg.aoff + j);
+                    const bool cac0 = __ldg(sc.coinc + qa0 + sg.aoff + j);
+                    const bool cac1 = __ldg(sc.coinc + qa1 + sg.aoff + j);
 #pragma unroll
-                    for (int k = 0; k < NM; ++k)
-                        R[k] = fminf(R[k], cand_value(e0[k], e0[NM], th_ab, arow[j], cbc || co_ab, cbc || cac,
-                                                      kc.c[k].z, kc.c[k].w, p.l23));
+                    for (int k = 0; k < NM; ++k) {
+                        R0[k] = fminf(R0[k], cand_value(e0[k], e0[NM], th_ab0, arow0[j], cbc || co_ab0, cbc || cac0,
+                                                        kc.c[k].z, kc.c[k].w, p.l23));
+                        R1[k] = fminf(R1[k], cand_value(e0[k], e0[NM], th_ab1, arow1[j], cbc || co_ab1, cbc || cac1,
+                                                        kc.c[k].z, kc.c[k].w, p.l23));
+                    }
                 }
             }
             if (live) {
-                float out[EPF];
+                float out0[EPF], out1[EPF];
 #pragma unroll
                 for (int k = 0; k < NM; ++k) {
-                    const float real = __fadd_rn(R[k], state_const(p.l2, kc.c[k].y, sg.g));
-                    out[k] = fminf(real, b_ean[(b - B0) * NM + k]);
+                    const float sc_g = state_const(p.l2, kc.c[k].y, sg.g);  // same frame gap for both states
+                    const float ean = b_ean[(b - B0) * NM + k];
+                    out0[k] = fminf(__fadd_rn(R0[k], sc_g), ean);
+                    out1[k] = fminf(__fadd_rn(R1[k], sc_g), ean);
                 }
 #pragma unroll
-                for (int k = NM; k < EPF; ++k) out[k] = 0.f;
-                float4 *dst = reinterpret_cast<float4 *>(cur + (int64_t)(r_qp[ra] + colb - d.ppad) * EPF);
+                for (int k = NM; k < EPF; ++k) out0[k] = out1[k] = 0.f;
+                float4 *dst0 = reinterpret_cast<float4 *>(cur + (int64_t)(r_qp[ra0] + colb - d.ppad) * EPF);
 #pragma unroll
-                for (int q = 0; q < EPF / 4; ++q) dst[q] = make_float4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]);
+                for (int q = 0; q < EPF / 4; ++q)
+                    dst0[q] = make_float4(out0[4 * q], out0[4 * q + 1], out0[4 * q + 2], out0[4 * q + 3]);
+                if (two) {
+                    float4 *dst1 = reinterpret_cast<float4 *>(cur + (int64_t)(r_qp[ra1] + colb - d.ppad) * EPF);
+#pragma unroll
+                    for (int q = 0; q < EPF / 4; ++q)
+                        dst1[q] = make_float4(out1[4 * q], out1[4 * q + 1], out1[4 * q + 2], out1[4 * q + 3]);
+                }
             }
         }
-        compute_sync();  // stage s and the item's bookkeeping are free again
-        if (tid == 0) mbar_arrive(&ctl->free_[s]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ctl->free_[s]);  // this warp is done with stage s
         if (tid == 0) trace(m, 3);
     }
 }
@@ -626,7 +709,7 @@ __global__ void __launch_bounds__(256) k_item_prep(SceneView sc, const WorkItem 
             sg.trip = max(0, min(sc.first(f - g + T), w.d.we) - c0);
             sg.aoff = c0 - sg.f1a;
             sg.inv = sg.nb > 1 ? 0xffffffffu / (unsigned)sg.nb + 1u : 0u;  // ceil(2^32 / nb)
-            cnt = sg.nb * (sg.f1a - sg.a0);
+            cnt = sg.nb * ((sg.f1a - sg.a0 + 1) >> 1);  // lane tasks: one b, a pair of a's
         }
     }
     s_cnt[tid] = cnt;
@@ -656,6 +739,11 @@ hgm_status launch_item_prep(const SceneView &v, const WorkItem *items, int nitem
 }
 
 size_t item_book_bytes(const TileCaps &caps, int T) { return BookPlan(caps, T).total; }
+
+// stage bytes of an item of the given sizes (host tiling; the layout the kernel uses)
+size_t item_stage_bytes(int NE, int NTH, int NC, int NA, int NB, int FT, int T, int NM, int book) {
+    return (size_t)StageLayout(NE, NTH, NC, NA, NB, FT, T, NM, book).total;
+}
 
 // ------------------------------------------------------------------ launchers
 size_t dp_batch_smem(const TileCaps &c, int T, int NM) { return SmemPlan(c, T, NM).total; }

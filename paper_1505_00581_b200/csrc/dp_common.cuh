@@ -68,6 +68,7 @@ struct TileCaps {  // shared-memory capacities of one K-DP work item, maxima ove
     int NST;    // real states
     int FT;     // b-frames
     int W;      // window length in frames
+    int STAGE;  // bytes of one K-DP shared-memory stage (largest item layout)
 };
 
 // One K-DP work item: a tile of b-frames [F0, F1) of one window (dp_batch.cu).

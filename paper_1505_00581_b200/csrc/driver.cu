@@ -13,6 +13,7 @@ namespace hgm {
 hgm_status launch_item_prep(const SceneView &v, const WorkItem *items, int nitems, const TileCaps &caps, int T,
                             unsigned char *book, cudaStream_t s);
 size_t item_book_bytes(const TileCaps &caps, int T);
+size_t item_stage_bytes(int NE, int NTH, int NC, int NA, int NB, int FT, int T, int NM, int book);
 hgm_status launch_dp_batch(int NM, const SceneView &v, const WorkItem *items, int nitems, const unsigned char *book,
                            int *counter, float *hist, int64_t L, int layer, bool has_next, bool has_prev,
                            const StepConstB &kc, const float *U, int64_t ui_off, const DPParams &p,
@@ -73,48 +74,60 @@ static bool make_tiling(const hgm_scene *sc, const hgm_offsets &o, int T, int NM
     const int FT_max = std::max(1, std::min(8, 255 / std::max(1, T - 1)));
     const char *benv = getenv("HGM_SMEM_KB");  // tuning knob: shared memory per CTA (2 CTAs per SM by default)
     const size_t budgets[2] = {(size_t)(benv ? atoi(benv) : 110) * 1024, 220 * 1024};
-    const int64_t ent_bytes = 4 * 2 * entry_floats(NM);  // 2 stages of candidate entries
-    for (int bi = 0; bi < 2; ++bi)
-    for (int64_t cap = (int64_t)budgets[bi]; cap >= 4096; cap = cap * 7 / 8) {
-        const size_t budget = budgets[bi];
-        Tiling t;
-        t.f_lo = (int)f_lo;
-        TileCaps c{1, 1, 1, 1, 1, 1, 1, o.window};
-        bool ok = true;
-        for (int64_t F0 = f_lo; F0 < f_hi;) {
-            int64_t F1 = F0 + 1;
-            auto ne = [&](int64_t a, int64_t b) { return QP(b) - QP(a); };
-            auto th = [&](int64_t a, int64_t b) { return QP(b) - QP(a - T + 1) + 8; };
-            auto foot = [&](int64_t a, int64_t b) { return ent_bytes * ne(a, b) + 8 * th(a, b); };
-            while (F1 < f_hi && F1 - F0 < FT_max && foot(F0, F1 + 1) <= cap) ++F1;
-            t.gstart.push_back((int32_t)F0);
-            c.NE = (int)std::max<int64_t>(c.NE, ne(F0, F1));
-            c.TH = (int)std::max<int64_t>(c.TH, th(F0, F1));
-            c.NA = (int)std::max<int64_t>(c.NA, NF(F1) - NF(F0 - T + 1));
-            c.NB = (int)std::max<int64_t>(c.NB, NF(F1) - NF(F0));
-            c.NC = (int)std::max<int64_t>(c.NC, NF(F1 + T - 1) - NF(F0));
-            int64_t nst = 0;
-            for (int64_t f = F0; f < F1; ++f) nst += (NF(f + 1) - NF(f)) * (NF(f) - NF(f - T + 1));
-            c.NST = (int)std::max<int64_t>(c.NST, nst);
-            c.FT = (int)std::max<int64_t>(c.FT, F1 - F0);
-            F0 = F1;
+    auto foot = [&](int64_t a, int64_t b, int64_t book) {  // stage bytes of the unclipped tile [a, b)
+        return (int64_t)item_stage_bytes((int)(QP(b) - QP(a)), (int)(QP(b) - QP(a - T + 1)), (int)(NF(b + T - 1) - NF(a)),
+                                         (int)(NF(b) - NF(a - T + 1)), (int)(NF(b) - NF(a)), (int)(b - a), T, NM,
+                                         (int)book);
+    };
+    for (int bi = 0; bi < 2; ++bi) {
+        TileCaps c0{1, 1, 1, 1, 1, 1, FT_max, o.window, 0};
+        const int64_t fixed = (int64_t)dp_batch_smem(c0, T, NM);  // stage-independent part
+        const int64_t cap = ((int64_t)budgets[bi] - fixed) / 2 / 16 * 16;
+        int64_t book = (int64_t)item_book_bytes(c0, T);
+        for (int iter = 0; iter < 4; ++iter) {
+            Tiling t;
+            t.f_lo = (int)f_lo;
+            TileCaps c{1, 1, 1, 1, 1, 1, 1, o.window, 0};
+            for (int64_t F0 = f_lo; F0 < f_hi;) {
+                int64_t F1 = F0 + 1;  // a single frame is always a tile
+                while (F1 < f_hi && F1 - F0 < FT_max && foot(F0, F1 + 1, book) <= cap) ++F1;
+                t.gstart.push_back((int32_t)F0);
+                c.STAGE = (int)std::max<int64_t>(c.STAGE, foot(F0, F1, book));
+                c.NE = (int)std::max<int64_t>(c.NE, QP(F1) - QP(F0));
+                c.TH = (int)std::max<int64_t>(c.TH, QP(F1) - QP(F0 - T + 1) + 8);
+                c.NA = (int)std::max<int64_t>(c.NA, NF(F1) - NF(F0 - T + 1));
+                c.NB = (int)std::max<int64_t>(c.NB, NF(F1) - NF(F0));
+                c.NC = (int)std::max<int64_t>(c.NC, NF(F1 + T - 1) - NF(F0));
+                int64_t nst = 0;
+                for (int64_t f = F0; f < F1; ++f) nst += (NF(f + 1) - NF(f)) * (NF(f) - NF(f - T + 1));
+                c.NST = (int)std::max<int64_t>(c.NST, nst);
+                c.FT = (int)std::max<int64_t>(c.FT, F1 - F0);
+                F0 = F1;
+            }
+            c.FT = FT_max;  // the copy warp's frame-minima buffer is sized for FT_max
+            const int64_t need_book = (int64_t)item_book_bytes(c, T);
+            if (need_book > book) {  // the bookkeeping record grew: retile with it
+                book = need_book;
+                continue;
+            }
+            if (c.STAGE > cap || dp_batch_smem(c, T, NM) > budgets[bi]) break;  // a single frame exceeds this budget
+            const int ntiles = (int)t.gstart.size();
+            t.gstart.push_back((int32_t)f_hi);
+            t.tile_of.resize((size_t)(f_hi - f_lo));
+            for (int q = 0; q < ntiles; ++q)
+                for (int64_t f = t.gstart[q]; f < t.gstart[q + 1]; ++f) t.tile_of[f - f_lo] = q;
+            int slots = 1;
+            for (int k = 0; k < o.count; ++k) {
+                const int64_t of = (int64_t)o.first_frame + (int64_t)k * o.stride;
+                slots = std::max(slots, t.tile_of[of + o.window - 1 - f_lo] - t.tile_of[of - f_lo] + 1);
+            }
+            for (int q = 0; q <= slots; ++q) t.gstart.push_back(INT32_MAX / 2);
+            t.slots = slots;
+            c.STAGE = (int)std::max<int64_t>(c.STAGE, 16);
+            t.caps = c;
+            *tl = std::move(t);
+            return true;
         }
-        if (!ok || dp_batch_smem(c, T, NM) > budget) continue;
-        const int ntiles = (int)t.gstart.size();
-        t.gstart.push_back((int32_t)f_hi);
-        t.tile_of.resize((size_t)(f_hi - f_lo));
-        for (int q = 0; q < ntiles; ++q)
-            for (int64_t f = t.gstart[q]; f < t.gstart[q + 1]; ++f) t.tile_of[f - f_lo] = q;
-        int slots = 1;
-        for (int k = 0; k < o.count; ++k) {
-            const int64_t of = (int64_t)o.first_frame + (int64_t)k * o.stride;
-            slots = std::max(slots, t.tile_of[of + o.window - 1 - f_lo] - t.tile_of[of - f_lo] + 1);
-        }
-        for (int q = 0; q <= slots; ++q) t.gstart.push_back(INT32_MAX / 2);  // slots past the last tile: empty
-        t.slots = slots;
-        t.caps = c;
-        *tl = std::move(t);
-        return true;
     }
     return false;
 }

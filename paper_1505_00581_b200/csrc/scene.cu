@@ -67,7 +67,9 @@ __global__ void k_rowlen(int64_t S, int T_max, int fmax, const int32_t *__restri
 __global__ void k_padlen(int64_t S, const int32_t *__restrict__ rowlen, int32_t *padlen) {
     int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (a > S) return;
-    padlen[a] = a == S ? 0 : (rowlen[a] | 1);  // odd: consecutive rows on distinct banks
+    // padded length = 1 (mod 4): consecutive rows start in distinct 32-byte bank groups of
+    // K-DP's candidate entries (and on distinct 4-byte banks of its direction rows)
+    padlen[a] = a == S ? 0 : rowlen[a] + ((5 - (rowlen[a] & 3)) & 3);
 }
 
 // K-G: direction band theta(a->c) and coincidence flags, one thread per row a
@@ -101,9 +103,9 @@ __global__ void k_band(int64_t S, int T_max, int fmax, const int32_t *__restrict
             lc = c - lo;
         }
     }
-    if (((hi - lo) & 1) == 0) {  // padding slot
-        tp[hi - lo] = 0.f;
-        rp[hi - lo] = -1;
+    for (int q = hi - lo; q < qpad[a + 1] - qpad[a]; ++q) {  // padding slots
+        tp[q] = 0.f;
+        rp[q] = -1;
     }
     rfc[a] = fc;
     rlc[a] = lc;
