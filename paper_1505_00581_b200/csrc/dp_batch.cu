@@ -643,7 +643,7 @@ __global__ void k_init_ee(const InstDesc *__restrict__ inst, int ninst, float *_
 // every step of the chunk.
 __global__ void k_items(SceneView sc, const InstDesc *__restrict__ inst, int ninst, int W, int T,
                         const int32_t *__restrict__ gstart, const int32_t *__restrict__ tile_of, int tf_lo,
-                        const int32_t *__restrict__ item_base, WorkItem *items) {
+                        const int32_t *__restrict__ item_base, int base0, WorkItem *items) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= ninst) return;
     const InstDesc d = inst[k];
@@ -652,7 +652,7 @@ __global__ void k_items(SceneView sc, const InstDesc *__restrict__ inst, int nin
         WorkItem w{};
         w.d = d;
         w.live = 1;
-        w.idx = __ldg(item_base + k) + x;
+        w.idx = __ldg(item_base + k) - base0 + x;
         w.F0 = max(__ldg(gstart + g0 + x), d.o);
         w.F1 = min(__ldg(gstart + g0 + x + 1), d.o + W);
         w.B0 = sc.first(w.F0);
@@ -662,7 +662,7 @@ __global__ void k_items(SceneView sc, const InstDesc *__restrict__ inst, int nin
         w.qa = __ldg(sc.qpad + w.A0);
         w.qb0 = __ldg(sc.qpad + w.B0);
         w.qb1 = __ldg(sc.qpad + w.B1);
-        items[__ldg(item_base + k) + x] = w;
+        items[w.idx] = w;
     }
 }
 
@@ -817,9 +817,11 @@ hgm_status launch_dp_batch(int NM, const SceneView &v, const WorkItem *items, in
 }
 
 hgm_status launch_items(const SceneView &v, const InstDesc *dinst, int ninst, int W, int T, const int32_t *gstart,
-                        const int32_t *tile_of, int tf_lo, const int32_t *item_base, WorkItem *items, cudaStream_t s) {
+                        const int32_t *tile_of, int tf_lo, const int32_t *item_base, int base0, WorkItem *items,
+                        cudaStream_t s) {
     if (ninst > 0)
-        k_items<<<(ninst + 127) / 128, 128, 0, s>>>(v, dinst, ninst, W, T, gstart, tile_of, tf_lo, item_base, items);
+        k_items<<<(ninst + 127) / 128, 128, 0, s>>>(v, dinst, ninst, W, T, gstart, tile_of, tf_lo, item_base, base0,
+                                                    items);
     return HGM_OK;
 }
 

@@ -19,7 +19,8 @@ hgm_status launch_dp_batch(int NM, const SceneView &v, const WorkItem *items, in
                            const StepConstB &kc, const float *U, int64_t ui_off, const DPParams &p,
                            const TileCaps &caps, cudaStream_t s);
 hgm_status launch_items(const SceneView &v, const InstDesc *dinst, int ninst, int W, int T, const int32_t *gstart,
-                        const int32_t *tile_of, int tf_lo, const int32_t *item_base, WorkItem *items, cudaStream_t s);
+                        const int32_t *tile_of, int tf_lo, const int32_t *item_base, int base0, WorkItem *items,
+                        cudaStream_t s);
 hgm_status launch_init_ee(const InstDesc *dinst, int ninst, float *hist, int64_t L, int layer, int NM,
                           cudaStream_t s);
 size_t dp_batch_smem(const TileCaps &c, int T, int NM);
@@ -204,9 +205,8 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
     const int nlanes = (senv && atoi(senv) == 2) ? 2 : 1;
     struct Lane {
         cudaStream_t s = nullptr;
-        DevBuf hist, dinst, items, counters, ibase, book;
-        int64_t hist_cap = 0, dinst_cap = 0, items_cap = 0, counters_cap = 0, ibase_cap = 0, book_cap = 0;
-        std::vector<int32_t> ibase_h;
+        DevBuf hist, items, counters, book;
+        int64_t hist_cap = 0, items_cap = 0, counters_cap = 0, book_cap = 0;
     } lanes[2];
     lanes[0].s = s;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -214,62 +214,69 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
         lanes[1].s = aux_stream(sc->device);
         HGM_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
         HGM_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    }
+    // Chunks of windows (the alpha history of a chunk fits the budget), every window's
+    // layer offset and work-item count, planned up front so that the window
+    // descriptors and item prefixes reach the device in one copy each (no per-chunk
+    // pageable copies between the chunks' kernels).
+    struct Chunk {
+        int k0, k1, nitems;
+        int64_t L, maxNs;
+    };
+    std::vector<Chunk> chunks;
+    std::vector<int32_t> ibase_all((size_t)count + 1, 0);
+    int64_t max_hist = 4, max_items = 1;
+    for (int k0 = 0; k0 < count;) {
+        Chunk c{k0, k0, 0, 0, 1};
+        while (c.k1 < count && c.k1 - k0 < chunk_max) {
+            InstDesc &d = all[c.k1];
+            const int64_t ns = (int64_t)d.ntail + 2 * (int64_t)(d.we - d.wb) + 1;
+            if (c.k1 > k0 && (c.L + ns * SS) * std::max(nsteps, 1) > budget_floats) break;
+            d.off = c.L;
+            c.L += ns * SS;
+            c.maxNs = std::max(c.maxNs, ns);
+            if (!v0) {
+                const int of = d.o;
+                ibase_all[c.k1 + 1] = ibase_all[c.k1] + tl.tile_of[of + o.window - 1 - tl.f_lo] - tl.tile_of[of - tl.f_lo] + 1;
+            }
+            ++c.k1;
+        }
+        c.nitems = ibase_all[c.k1] - ibase_all[k0];
+        max_hist = std::max(max_hist, c.L * nsteps + 4);  // + 16 bytes: K-DP's bulk copies round to 16-byte units
+        max_items = std::max<int64_t>(max_items, c.nitems);
+        chunks.push_back(c);
+        k0 = c.k1;
+    }
+    DevBuf d_all, d_ibase;
+    HGM_TRY(d_all.alloc(sizeof(InstDesc) * count, s));
+    HGM_CUDA(cudaMemcpyAsync(d_all.p, all.data(), sizeof(InstDesc) * count, cudaMemcpyHostToDevice, s));
+    if (!v0) {
+        HGM_TRY(d_ibase.alloc(sizeof(int32_t) * (count + 1), s));
+        HGM_CUDA(cudaMemcpyAsync(d_ibase.p, ibase_all.data(), sizeof(int32_t) * (count + 1), cudaMemcpyHostToDevice, s));
+    }
+    if (nlanes == 2) {  // the second lane starts after the uploads
         HGM_CUDA(cudaEventRecord(ev_fork, s));
         HGM_CUDA(cudaStreamWaitEvent(lanes[1].s, ev_fork, 0));
     }
     hgm_status st = HGM_OK;
-    int chunk = 0;
-    for (int k0 = 0; k0 < count && st == HGM_OK; ++chunk) {
+    for (int chunk = 0; chunk < (int)chunks.size() && st == HGM_OK; ++chunk) {
+        const Chunk &ch = chunks[chunk];
         Lane &ln = lanes[chunk % nlanes];
         const cudaStream_t ls = ln.s;
-        int64_t L = 0, maxNs = 1;
-        int k1 = k0;
-        while (k1 < count && k1 - k0 < chunk_max) {
-            InstDesc &d = all[k1];
-            const int64_t ns = (int64_t)d.ntail + 2 * (int64_t)(d.we - d.wb) + 1;
-            if (k1 > k0 && (L + ns * SS) * std::max(nsteps, 1) > budget_floats) break;
-            d.off = L;
-            L += ns * SS;
-            maxNs = std::max(maxNs, ns);
-            ++k1;
+        const int k0 = ch.k0, ninst = ch.k1 - ch.k0;
+        const int64_t L = ch.L, maxNs = ch.maxNs;
+        cudaError_t e = cudaSuccess;
+        if (max_hist > ln.hist_cap) {
+            if ((st = ln.hist.alloc(sizeof(float) * max_hist, ls)) != HGM_OK) break;
+            ln.hist_cap = max_hist;
         }
-        const int ninst = k1 - k0;
-        if (ninst > ln.dinst_cap) {
-            if ((st = ln.dinst.alloc(sizeof(InstDesc) * ninst, ls)) != HGM_OK) break;
-            ln.dinst_cap = ninst;
-        }
-        cudaError_t e = cudaMemcpyAsync(ln.dinst.p, all.data() + k0, sizeof(InstDesc) * ninst,
-                                        cudaMemcpyHostToDevice, ls);
-        if (e != cudaSuccess) {
-            st = cuda_fail(e, "cudaMemcpyAsync(instances)");
-            break;
-        }
-        const int64_t need = L * nsteps + 4;  // + 16 bytes: K-DP's bulk copies round ranges to 16-byte units
-        if (need > ln.hist_cap) {
-            if ((st = ln.hist.alloc(sizeof(float) * need, ls)) != HGM_OK) break;
-            ln.hist_cap = need;
-        }
-        const InstDesc *di = ln.dinst.as<InstDesc>();
+        const InstDesc *di = d_all.as<InstDesc>() + k0;
         float *hist = ln.hist.as<float>();
-        int nitems = 0;
+        const int nitems = ch.nitems;
         if (!v0 && nsteps > 0) {
-            // work items of each window: the tiles meeting its frames (host prefix, device fill)
-            ln.ibase_h.resize(ninst + 1);
-            ln.ibase_h[0] = 0;
-            for (int k = 0; k < ninst; ++k) {
-                const int of = all[k0 + k].o;
-                ln.ibase_h[k + 1] = ln.ibase_h[k] + tl.tile_of[of + o.window - 1 - tl.f_lo] - tl.tile_of[of - tl.f_lo] + 1;
-            }
-            nitems = ln.ibase_h[ninst];
-            if (ninst + 1 > ln.ibase_cap) {
-                if ((st = ln.ibase.alloc(sizeof(int32_t) * (ninst + 1), ls)) != HGM_OK) break;
-                ln.ibase_cap = ninst + 1;
-            }
-            HGM_CUDA(cudaMemcpyAsync(ln.ibase.p, ln.ibase_h.data(), sizeof(int32_t) * (ninst + 1), cudaMemcpyHostToDevice,
-                                     ls));
-            if (nitems > ln.items_cap) {
-                if ((st = ln.items.alloc(sizeof(WorkItem) * nitems, ls)) != HGM_OK) break;
-                ln.items_cap = nitems;
+            if (max_items > ln.items_cap) {
+                if ((st = ln.items.alloc(sizeof(WorkItem) * max_items, ls)) != HGM_OK) break;
+                ln.items_cap = max_items;
             }
             if (nsteps > ln.counters_cap) {
                 if ((st = ln.counters.alloc(sizeof(int) * nsteps, ls)) != HGM_OK) break;
@@ -277,8 +284,8 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
             }
             HGM_CUDA(cudaMemsetAsync(ln.counters.p, 0, sizeof(int) * nsteps, ls));
             launch_items(v, di, ninst, o.window, p.T, d_gstart.as<int32_t>(), d_tile_of.as<int32_t>(), tl.f_lo,
-                         ln.ibase.as<int32_t>(), ln.items.as<WorkItem>(), ls);
-            const int64_t bbytes = (int64_t)item_book_bytes(tl.caps, p.T) * nitems + 16;
+                         d_ibase.as<int32_t>() + k0, ibase_all[k0], ln.items.as<WorkItem>(), ls);
+            const int64_t bbytes = (int64_t)item_book_bytes(tl.caps, p.T) * max_items + 16;
             if (bbytes > ln.book_cap) {
                 if ((st = ln.book.alloc(bbytes, ls)) != HGM_OK) break;
                 ln.book_cap = bbytes;
@@ -324,7 +331,6 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
             count_launch(K_BT);
         }
         if (st == HGM_OK && (e = cudaGetLastError()) != cudaSuccess) st = cuda_fail(e, "K-BT launch");
-        k0 = k1;  // a lane's buffers are reused by its next chunk: stream order protects them
     }
     if (nlanes == 2) {  // join: the caller's stream waits for the second lane
         cudaEventRecord(ev_join, lanes[1].s);
