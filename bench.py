@@ -41,6 +41,10 @@ sys.path.insert(0, ROOT)
 BASELINE_METRIC = "matched (model, offset) pairs/sec and frames/sec at 1/2/4/8 B200; % ALU roofline"
 ISSUE_SLOTS_PER_CAND = 10.5  # 6 FADD + FMUL + FFMA + MUFU + FFMA + 1/2 FMNMX3
 LANES_PER_CLK = 148 * 4 * 32  # 148 SMs x 4 SMSPs x 32 lanes
+# XU (MUFU) pipe: 0.497 warp-instructions / clk / SM measured for MUFU.SQRT on this pool's
+# B200 (tools/pipe_microbench.cu, profiles/r01_pipe_microbench.txt) = 15.9 lanes / clk / SM;
+# every model-candidate needs one square root (Eq. 6's norm), so this is a second, tighter bound.
+XU_LANES_PER_CLK = 148 * 0.497 * 32
 
 
 def parse():
@@ -277,6 +281,7 @@ def main():
     f_mhz = ck["sm_mhz"] or 1965.0
     achieved = work_cand / (dp_ms / 1000.0) / 1e9  # G real-triple candidates / s
     peak = LANES_PER_CLK * f_mhz * 1e6 / ISSUE_SLOTS_PER_CAND / 1e9
+    xu_peak = XU_LANES_PER_CLK * f_mhz * 1e6 / 1e9  # G model-candidates / s (one MUFU.SQRT each)
     traffic, traffic_src = None, None
     tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "dp_traffic.json")
     if os.path.exists(tpath):  # DRAM bytes per K-DP launch from the committed ncu --set full capture
@@ -285,7 +290,9 @@ def main():
         traffic, traffic_src = tj.get("dram_bytes_per_launch"), tj.get("source")
     roof = dict(bound="alu", achieved=achieved, peak=peak, unit="Gcand/s", frac=achieved / peak, traffic=traffic,
                 traffic_unit="DRAM bytes per K-DP launch", traffic_source=traffic_src,
-                kernel="k_dp_batch", dp_ms_per_step=dp_ms, dp_share_of_step=dp_ms / ms_step,
+                xu_peak=xu_peak, xu_frac=achieved / xu_peak,
+                xu_basis="one MUFU.SQRT per model-candidate; 148 SMs x 15.9 lanes/clk (measured) x SM clock",
+                kernel="k_dp_fused", dp_ms_per_step=dp_ms, dp_share_of_step=dp_ms / ms_step,
                 candidates_per_step=work_cand, states_per_step=work_states,
                 peak_basis=f"148 SMs x 128 lanes x {f_mhz:.0f} MHz (median SM clock sampled in the timed region)"
                            f" / {ISSUE_SLOTS_PER_CAND} issue slots per real-triple candidate",

@@ -148,18 +148,21 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-// Spin on test_wait (never suspends: a suspended try_wait was seen to oversleep the
-// phase completion by up to milliseconds); the spin is a few instructions per probe.
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
-    unsigned ok = 0;
+// Poll test_wait with exponential back-off (__nanosleep 64 ns .. max_ns): a suspended
+// try_wait was seen to oversleep the phase completion by up to milliseconds, and a
+// tight poll costs issue slots the working warps need.
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity, unsigned max_ns = 512) {
+    unsigned ns = 64;
     for (;;) {
+        unsigned ok;
         asm volatile(
             "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
             : "=r"(ok)
             : "r"(smem_u32(bar)), "r"(parity)
             : "memory");
         if (ok) break;
-        __nanosleep(32);
+        __nanosleep(ns);
+        ns = min(2 * ns, max_ns);
     }
 }
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
@@ -354,14 +357,22 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
     if (warp == KDP_WARPS) {
         // ---------------- copy warp: item m goes to stage m % 2 once item m-2 left it; it
         // also computes the dummy-form states (eps, b) and (eps, eps) of each item
+        // lane 0 claims one item ahead: the claim and the descriptor load of item m+1 are in
+        // flight while item m-1 still occupies the stage item m+1 will use
+        int next_idx = lane == 0 ? atomicAdd(counter, 1) : 0;
         for (int m = 0;; ++m) {
             const int st = m & 1;
-            if (m >= 2) mbar_wait(&ctl->free_[st], ((m - 2) >> 1) & 1);
+            WorkItem pre{};
             if (lane == 0) {
-                const int idx = atomicAdd(counter, 1);
+                if (next_idx < nitems) pre = items[next_idx];
+                next_idx = next_idx < nitems ? atomicAdd(counter, 1) : nitems;
+            }
+            if (m >= 2) mbar_wait(&ctl->free_[st], ((m - 2) >> 1) & 1, 2048);
+            if (lane == 0) trace(m, 4);
+            if (lane == 0) {
                 WorkItem &nw = ctl->w[st];
-                if (idx < nitems) {
-                    nw = items[idx];
+                if (pre.live) {
+                    nw = pre;
                     ctl->lay[st] = item_layout(nw, T, NM, (int)bp.total);
                     ctl->row_claim[st] = 0;
                     ctl->task_claim[st] = 0;
@@ -370,12 +381,14 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
                                  : "memory");
                     issue_stage<NM, kHasNext>(sc, nw, hist, L, layer, U, ui_off, T, sp, smem, st, &ctl->raw[st], book,
                                               (unsigned)bp.total);
+                    trace(m, 5);
                 } else {
                     nw.live = 0;
                     mbar_arrive(&ctl->raw[st]);
                 }
             }
             mbar_wait(&ctl->raw[st], (m >> 1) & 1);
+            if (lane == 0) trace(m, 6);
             const WorkItem &w = ctl->w[st];
             if (!w.live) break;
             const InstDesc &d = w.d;

@@ -293,7 +293,7 @@ def set_profiling(enable: bool = True):
 def get_stats(reset: bool = False) -> dict:
     s = Stats()
     _check(lib().hgm_get_stats(C.byref(s), int(bool(reset))))
-    names = ("scene", "model", "unary", "dp", "backtrack", "argmin", "msg", "reserved")
+    names = ("scene", "model", "unary", "dp", "backtrack", "argmin", "unused", "reserved")
     return dict(ms={n: s.ms[i] for i, n in enumerate(names)},
                 launches={n: s.launches[i] for i, n in enumerate(names)}, dp_launches=s.dp_launches)
 
