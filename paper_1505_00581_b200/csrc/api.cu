@@ -47,15 +47,29 @@ struct Pending {
     cudaEvent_t a, b;
 };
 std::vector<Pending> g_pending;
+std::vector<cudaEvent_t> g_event_pool;  // events are reused: creating thousands per step stalls the host
 hgm_stats g_stats{};
+cudaEvent_t take_event() {  // g_mu held
+    if (!g_event_pool.empty()) {
+        cudaEvent_t e = g_event_pool.back();
+        g_event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
 }  // namespace
 
 bool profiling() { return g_prof; }
 
 Timer::Timer(cudaStream_t s_, int cls_) : s(s_), cls(cls_) {
     if (!g_prof) return;
-    cudaEventCreate(&a);
-    cudaEventCreate(&b);
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        a = take_event();
+        b = take_event();
+    }
     cudaEventRecord(a, s);
 }
 Timer::~Timer() {
@@ -425,8 +439,8 @@ hgm_status hgm_get_stats(hgm_stats *out, int reset) {
         cudaEventSynchronize(pe.b);
         cudaEventElapsedTime(&ms, pe.a, pe.b);
         g_stats.ms[pe.cls] += ms;
-        cudaEventDestroy(pe.a);
-        cudaEventDestroy(pe.b);
+        g_event_pool.push_back(pe.a);
+        g_event_pool.push_back(pe.b);
     }
     g_pending.clear();
     *out = g_stats;

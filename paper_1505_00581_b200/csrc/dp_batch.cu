@@ -148,22 +148,18 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-// Poll test_wait with exponential back-off (__nanosleep 64 ns .. max_ns): a suspended
-// try_wait was seen to oversleep the phase completion by up to milliseconds, and a
-// tight poll costs issue slots the working warps need.
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity, unsigned max_ns = 512) {
-    unsigned ns = 64;
-    for (;;) {
-        unsigned ok;
+// try_wait with a short suspend-time hint: the waiting warp sleeps in hardware (no
+// polling instructions) and oversleeps the phase completion by at most ~hint_ns (a
+// 1 ms hint was seen to oversleep by that much).
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity, unsigned hint_ns = 256) {
+    unsigned ok = 0;
+    do {
         asm volatile(
-            "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
             : "=r"(ok)
-            : "r"(smem_u32(bar)), "r"(parity)
+            : "r"(smem_u32(bar)), "r"(parity), "r"(hint_ns)
             : "memory");
-        if (ok) break;
-        __nanosleep(ns);
-        ns = min(2 * ns, max_ns);
-    }
+    } while (!ok);
 }
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -367,7 +363,7 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
                 if (next_idx < nitems) pre = items[next_idx];
                 next_idx = next_idx < nitems ? atomicAdd(counter, 1) : nitems;
             }
-            if (m >= 2) mbar_wait(&ctl->free_[st], ((m - 2) >> 1) & 1, 2048);
+            if (m >= 2) mbar_wait(&ctl->free_[st], ((m - 2) >> 1) & 1, 1024);
             if (lane == 0) trace(m, 4);
             if (lane == 0) {
                 WorkItem &nw = ctl->w[st];
