@@ -85,42 +85,62 @@ def rank_workload(name, rank, world, frames_per_gpu):
 
 # --------------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock, power and clock-event reasons sampled in-process through NVML
+    (nvidia_ml_py) every 500 ms while the timed region runs.  (A polling nvidia-smi
+    subprocess intermittently stalled the GPU work by 100-1000 ms.)"""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, gpu_index):
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        import threading
+
+        self.rows, self.stop_flag, self.t = [], False, None
+        self.nv = None
+        self.active = False  # samples are kept only between begin() and stop()
+        if os.environ.get("HGM_NO_CLOCKS"):  # diagnosis only: no sampling at all
+            return
         try:
-            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                       "-lms", "200", "-i", str(gpu_index)], stdout=self.f, stderr=subprocess.DEVNULL)
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(int(gpu_index))
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
         except Exception:
-            self.p = None
+            self.nv = None
+            return
+
+        def run():
+            import time as _t
+
+            while not self.stop_flag:
+                try:
+                    sm = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+                    pw = self.nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0
+                    rs = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                    if self.active:
+                        self.rows.append((sm, pw, rs))
+                except Exception:
+                    pass
+                _t.sleep(0.5)
+
+        self.t = threading.Thread(target=run, daemon=True)
+        self.t.start()
+
+    def begin(self):
+        self.active = True
 
     def stop(self):
-        if self.p is not None:
-            self.p.terminate()
-            try:
-                self.p.wait(timeout=5)
-            except Exception:
-                self.p.kill()
-        self.f.flush()
-        rows = []
-        with open(self.f.name) as fh:
-            for line in fh:
-                parts = [x.strip() for x in line.split(",")]
-                if len(parts) >= 9:
-                    rows.append(parts)
-        os.unlink(self.f.name)
-        if not rows:
+        self.active = False
+        self.stop_flag = True
+        if self.t is not None:
+            self.t.join(timeout=2)
+        if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[j] for r in rows for j in range(4) if r[5 + j].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows),
-                "power_w_max": max((float(r[3]) for r in rows if r[3].replace(".", "").isdigit()), default=None)}
+        reasons = sorted({n for _, _, r in self.rows for n, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.rows),
+                "power_w_max": max(r[1] for r in self.rows), "source": "NVML, 500 ms"}
 
 
 # --------------------------------------------------------------------- oracle
@@ -233,17 +253,19 @@ def main():
     work_cand = wk.real_candidates * steps_per_pair
     work_states = (wk.real_states + wk.eps_states) * steps_per_pair
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    hgm.set_profiling(True)
-    hgm.get_stats(reset=True)
     gpu_idx = local
     cvd = os.environ.get("CUDA_VISIBLE_DEVICES")
     if cvd:
         gpu_idx = cvd.split(",")[local]
-    clocks = ClockSampler(gpu_idx)
-    time.sleep(0.3)
+    clocks = ClockSampler(gpu_idx)  # started before the warm-up: its first NVML queries are slow
+    for w_ in range(args.warmup):
+        if w_ == args.warmup - 1:
+            hgm.set_profiling(True)  # the last warm-up step already runs with the event timers on
+        step()
+    torch.cuda.synchronize()
+    hgm.set_profiling(True)
+    hgm.get_stats(reset=True)
+    clocks.begin()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -251,15 +273,26 @@ def main():
     ev1 = torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()
     ev0.record()
+    dbg = os.environ.get("HGM_BENCH_DEBUG")
+    evs = []
     for _ in range(args.steps):
         flush.zero_()  # L2 flush between steps (counted inside the timed region)
         step()
+        if dbg:
+            evs.append(torch.cuda.Event(enable_timing=True))
+            evs[-1].record()
+            torch.cuda.synchronize()
+            st_ = hgm.get_stats(reset=False)
+            print("  cumulative kernel ms:", {k: round(v, 1) for k, v in st_["ms"].items() if v}, file=sys.stderr)
     ev1.record()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     wall = time.perf_counter() - t0
     ms = ev0.elapsed_time(ev1)
+    if dbg:
+        marks = [ev0] + evs
+        print("per-step ms:", [round(marks[j].elapsed_time(marks[j + 1]), 1) for j in range(len(evs))], file=sys.stderr)
     ck = clocks.stop()
     st = hgm.get_stats(reset=True)
     hgm.set_profiling(False)
@@ -332,18 +365,28 @@ def main():
                 torch.cuda.synchronize()
             return scene, models
 
-        step_e2e()
+        for _ in range(max(2, min(args.warmup, 3))):
+            step_e2e()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        ne = max(1, min(args.steps, 3))
+        ne = max(1, args.steps)
+        eev = []
         for _ in range(ne):
             flush.zero_()
             step_e2e()
+            if dbg:
+                eev.append(torch.cuda.Event(enable_timing=True))
+                eev[-1].record()
         e1.record()
+        if dbg:
+            torch.cuda.synchronize()
+            marks = [e0] + eev
+            print("e2e per-step ms:", [round(marks[j].elapsed_time(marks[j + 1]), 1) for j in range(len(eev))],
+                  file=sys.stderr)
         torch.cuda.synchronize()
         me = torch.tensor([e0.elapsed_time(e1) / ne], dtype=torch.float64, device=dev)
         if world > 1:

@@ -203,11 +203,18 @@ struct DevPoints {
     }
 };
 
-struct StreamGuard {  // a private stream for the synchronous host-input builders
+// A persistent private stream per device for the synchronous host-input builders
+// (creating and destroying a stream per call stalled the host now and then).
+static cudaStream_t builder_stream(int device) {
+    static std::mutex mu;
+    static cudaStream_t bs[64] = {};
+    std::lock_guard<std::mutex> lk(mu);
+    const int d = device < 0 || device >= 64 ? 0 : device;
+    if (!bs[d]) cudaStreamCreateWithFlags(&bs[d], cudaStreamNonBlocking);
+    return bs[d];
+}
+struct StreamGuard {
     cudaStream_t s = nullptr;
-    ~StreamGuard() {
-        if (s) cudaStreamDestroy(s);
-    }
 };
 
 // Keep freed stream-ordered allocations in the device pool (no release to the
@@ -224,6 +231,16 @@ static void configure_pool() {
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
         uint64_t thr = UINT64_MAX;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        // Pre-map 4 GiB into the pool once: later per-call allocations (point copies, scene
+        // arrays, unary tables) are carved from memory that is already mapped instead of
+        // mapping fresh pages mid-call (seen as 100-1000 ms host stalls).
+        cudaStream_t st = nullptr;
+        if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess) {
+            void *p = nullptr;
+            if (cudaMallocAsync(&p, (size_t)4 << 30, st) == cudaSuccess) cudaFreeAsync(p, st);
+            cudaStreamSynchronize(st);
+            cudaStreamDestroy(st);
+        }
     }
     cudaGetLastError();
     done[dev] = true;
@@ -247,7 +264,7 @@ hgm_status hgm_build_model_graph(const hgm_points *pts, int device, hgm_model **
     HGM_CUDA(cudaSetDevice(device));
     configure_pool();
     StreamGuard sg;
-    HGM_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+    sg.s = builder_stream(device);
     hgm_status st;
     {
         DevPoints dp;
@@ -284,7 +301,7 @@ hgm_status hgm_build_scene_index(const hgm_points *pts, int device, int32_t T_ma
     HGM_CUDA(cudaSetDevice(device));
     configure_pool();
     StreamGuard sg;
-    HGM_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+    sg.s = builder_stream(device);
     hgm_status st;
     {
         DevPoints dp;
@@ -428,6 +445,12 @@ hgm_status hgm_detect_actions(const hgm_model *const *models, int32_t n_models, 
 hgm_status hgm_set_profiling(int enable) {
     std::lock_guard<std::mutex> lk(g_mu);
     g_prof = enable != 0;
+    while (g_prof && g_event_pool.size() < 1024) {  // pre-create: no event creation inside timed regions
+        cudaEvent_t e = nullptr;
+        if (cudaEventCreate(&e) != cudaSuccess) break;
+        g_event_pool.push_back(e);
+    }
+    cudaGetLastError();
     return HGM_OK;
 }
 

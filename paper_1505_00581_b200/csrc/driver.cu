@@ -3,6 +3,7 @@
 // alpha history, one K-DP launch per recursion step i = M..3 (Eq. 10, the
 // paper's host loop of Alg. 2 with the whole batch of windows per launch), then K-BT.
 #include <algorithm>
+#include <memory>
 #include <cstdlib>
 #include <cstring>
 
@@ -46,6 +47,48 @@ static cudaStream_t aux_stream(int device) {
     if (device < 0 || device >= 64) return nullptr;
     if (!as[device]) cudaStreamCreateWithFlags(&as[device], cudaStreamNonBlocking);
     return as[device];
+}
+
+// Per-device cache of K-DP's large scratch buffers (alpha history, work items, item
+// bookkeeping, counters).  Allocating gigabytes per call from the stream-ordered pool maps
+// fresh pages whenever the previous call's free is not yet known complete on the new
+// call's stream (host-API calls use a fresh stream each), which made calls erratic.  A
+// call waits for the previous user's work (event) before touching the buffers and
+// records its own completion; buffers only grow.
+struct Scratch {
+    void *p = nullptr;
+    size_t cap = 0;
+    hgm_status ensure(size_t bytes) {
+        if (bytes <= cap) return HGM_OK;
+        if (p) cudaFree(p);  // synchronous, but rare (growth only)
+        p = nullptr;
+        cap = 0;
+        const size_t want = bytes + bytes / 4;
+        if (cudaMalloc(&p, want) != cudaSuccess) {
+            cudaGetLastError();
+            if (cudaMalloc(&p, bytes) != cudaSuccess) {
+                p = nullptr;
+                return cuda_fail(cudaGetLastError(), "cudaMalloc(K-DP scratch)");
+            }
+            cap = bytes;
+            return HGM_OK;
+        }
+        cap = want;
+        return HGM_OK;
+    }
+};
+struct ScratchSet {
+    std::mutex mu;
+    Scratch hist, items, book, counters;
+    cudaEvent_t done = nullptr;
+};
+static ScratchSet &scratch_set(int device) {
+    static std::mutex mu;
+    static ScratchSet *sets[64] = {};
+    std::lock_guard<std::mutex> lk(mu);
+    const int d = device < 0 || device >= 64 ? 0 : device;
+    if (!sets[d]) sets[d] = new ScratchSet();
+    return *sets[d];
 }
 
 bool use_v0_kernels() {
@@ -258,6 +301,10 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
         HGM_CUDA(cudaEventRecord(ev_fork, s));
         HGM_CUDA(cudaStreamWaitEvent(lanes[1].s, ev_fork, 0));
     }
+    ScratchSet &scr = scratch_set(sc->device);
+    std::unique_lock<std::mutex> scr_lock(scr.mu);  // held while this call enqueues work on the buffers
+    if (!scr.done) HGM_CUDA(cudaEventCreateWithFlags(&scr.done, cudaEventDisableTiming));
+    HGM_CUDA(cudaStreamWaitEvent(s, scr.done, 0));  // the previous user's kernels are done with them
     hgm_status st = HGM_OK;
     for (int chunk = 0; chunk < (int)chunks.size() && st == HGM_OK; ++chunk) {
         const Chunk &ch = chunks[chunk];
@@ -266,38 +313,61 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
         const int k0 = ch.k0, ninst = ch.k1 - ch.k0;
         const int64_t L = ch.L, maxNs = ch.maxNs;
         cudaError_t e = cudaSuccess;
-        if (max_hist > ln.hist_cap) {
-            if ((st = ln.hist.alloc(sizeof(float) * max_hist, ls)) != HGM_OK) break;
-            ln.hist_cap = max_hist;
+        float *hist = nullptr;
+        if (chunk % nlanes == 0) {
+            if ((st = scr.hist.ensure(sizeof(float) * max_hist)) != HGM_OK) break;
+            hist = static_cast<float *>(scr.hist.p);
+        } else {
+            if (max_hist > ln.hist_cap) {
+                if ((st = ln.hist.alloc(sizeof(float) * max_hist, ls)) != HGM_OK) break;
+                ln.hist_cap = max_hist;
+            }
+            hist = ln.hist.as<float>();
         }
         const InstDesc *di = d_all.as<InstDesc>() + k0;
-        float *hist = ln.hist.as<float>();
         const int nitems = ch.nitems;
+        WorkItem *items_p = nullptr;
+        int *counters_p = nullptr;
+        unsigned char *book_p = nullptr;
         if (!v0 && nsteps > 0) {
-            if (max_items > ln.items_cap) {
-                if ((st = ln.items.alloc(sizeof(WorkItem) * max_items, ls)) != HGM_OK) break;
-                ln.items_cap = max_items;
-            }
-            if (nsteps > ln.counters_cap) {
-                if ((st = ln.counters.alloc(sizeof(int) * nsteps, ls)) != HGM_OK) break;
-                ln.counters_cap = nsteps;
-            }
-            HGM_CUDA(cudaMemsetAsync(ln.counters.p, 0, sizeof(int) * nsteps, ls));
-            launch_items(v, di, ninst, o.window, p.T, d_gstart.as<int32_t>(), d_tile_of.as<int32_t>(), tl.f_lo,
-                         d_ibase.as<int32_t>() + k0, ibase_all[k0], ln.items.as<WorkItem>(), ls);
             const int64_t bbytes = (int64_t)item_book_bytes(tl.caps, p.T) * max_items + 16;
-            if (bbytes > ln.book_cap) {
-                if ((st = ln.book.alloc(bbytes, ls)) != HGM_OK) break;
-                ln.book_cap = bbytes;
+            if (chunk % nlanes == 0) {
+                if ((st = scr.items.ensure(sizeof(WorkItem) * max_items)) != HGM_OK) break;
+                if ((st = scr.counters.ensure(sizeof(int) * nsteps)) != HGM_OK) break;
+                if ((st = scr.book.ensure(bbytes)) != HGM_OK) break;
+                items_p = static_cast<WorkItem *>(scr.items.p);
+                counters_p = static_cast<int *>(scr.counters.p);
+                book_p = static_cast<unsigned char *>(scr.book.p);
+            } else {
+                if (max_items > ln.items_cap) {
+                    if ((st = ln.items.alloc(sizeof(WorkItem) * max_items, ls)) != HGM_OK) break;
+                    ln.items_cap = max_items;
+                }
+                if (nsteps > ln.counters_cap) {
+                    if ((st = ln.counters.alloc(sizeof(int) * nsteps, ls)) != HGM_OK) break;
+                    ln.counters_cap = nsteps;
+                }
+                if (bbytes > ln.book_cap) {
+                    if ((st = ln.book.alloc(bbytes, ls)) != HGM_OK) break;
+                    ln.book_cap = bbytes;
+                }
+                items_p = ln.items.as<WorkItem>();
+                counters_p = ln.counters.as<int>();
+                book_p = ln.book.as<unsigned char>();
             }
-            launch_item_prep(v, ln.items.as<WorkItem>(), nitems, tl.caps, p.T, ln.book.as<unsigned char>(), ls);
+            HGM_CUDA(cudaMemsetAsync(counters_p, 0, sizeof(int) * nsteps, ls));
+            launch_items(v, di, ninst, o.window, p.T, d_gstart.as<int32_t>(), d_tile_of.as<int32_t>(), tl.f_lo,
+                         d_ibase.as<int32_t>() + k0, ibase_all[k0], items_p, ls);
+            launch_item_prep(v, items_p, nitems, tl.caps, p.T, book_p, ls);
             launch_init_ee(di, ninst, hist, L, nsteps - 1, NM, ls);  // first layer's (eps, eps) slots
             count_launch(K_DP, 3);
         }
+        // one timer around the chunk's consecutive K-DP launches (M-2 of them): nothing
+        // else runs on the stream in between
+        std::unique_ptr<Timer> dp_timer(nsteps > 0 ? new Timer(ls, K_DP) : nullptr);
         for (int i = M - 1; i >= 2 && st == HGM_OK; --i) {
             const bool has_next = i + 1 <= M - 1;
             if (v0) {
-                Timer tm(ls, K_DP);
                 const float4 h = models[0]->step_h[i];
                 const StepConst kc{h.x, h.y, h.z, h.w};
                 st = launch_dp_v0(v, di, ninst, maxNs, hist, L, i - 2, has_next, kc, U + (int64_t)i * nn, n_lo, p, ls);
@@ -311,14 +381,11 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
                 kc.nA1[q] = make_float2(-kc.c[2 * q].z, -kc.c[k1].z);
                 kc.nK2[q] = make_float2(-kc.c[2 * q].w, -kc.c[k1].w);
             }
-            {
-                Timer tm(ls, K_DP);
-                st = launch_dp_batch(NM, v, ln.items.as<WorkItem>(), nitems, ln.book.as<unsigned char>(), ln.counters.as<int>() + (i - 2), hist,
-                                     L, i - 2, has_next, /*has_prev=*/i - 1 >= 2, kc, U,
-                                     ((int64_t)i * nn - n_lo) * NM, p, tl.caps, ls);
-                count_launch(K_DP);
-            }
+            st = launch_dp_batch(NM, v, items_p, nitems, book_p, counters_p + (i - 2), hist, L, i - 2, has_next,
+                                 /*has_prev=*/i - 1 >= 2, kc, U, ((int64_t)i * nn - n_lo) * NM, p, tl.caps, ls);
+            count_launch(K_DP);
         }
+        dp_timer.reset();
         if (st != HGM_OK) break;
         if ((e = cudaGetLastError()) != cudaSuccess) {
             st = cuda_fail(e, "K-DP launch");
@@ -338,6 +405,7 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
         cudaEventDestroy(ev_fork);
         cudaEventDestroy(ev_join);
     }
+    cudaEventRecord(scr.done, s);  // the next user of the scratch buffers waits for this call's kernels
     return st;
 }
 
