@@ -1,5 +1,5 @@
 // backtrack.cu -- K-BT: Eq. 13 init search + Eq. 12 backtrack + appearance
-// distance, one warp per (model, window) pair.
+// distance, one CTA per window, one warp per model.
 //
 // The argmin tables beta_i of Eq. 12 are not stored by K-DP.  For the one state
 // (z_{i-1}, z_{i-2}) the backtrack visits at step i, the warp re-evaluates the
@@ -9,6 +9,8 @@
 // The arithmetic being identical, the minimum found here is bit-identical to
 // the alpha value K-DP stored, so the returned assignment is exactly the one
 // the stored beta table would have produced.
+#include <algorithm>
+
 #include "dp_common.cuh"
 
 namespace hgm {
@@ -23,65 +25,100 @@ __device__ __forceinline__ bool better(const Best &x, const Best &y) {  // lexic
     return x.z2 < y.z2;
 }
 
-__global__ void __launch_bounds__(128) k_backtrack_warp(SceneView sc, const InstDesc *__restrict__ inst, int npairs,
-                                                        const float *__restrict__ hist, int64_t L, BTArgs bt,
-                                                        DPParams p) {
-    const int lane = threadIdx.x & 31;
-    const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (wid >= npairs) return;
-    const int NM = bt.NM, kk = wid % NM;
-    const InstDesc d = inst[wid / NM];
-    const int Sw = d.we - d.wb, M = bt.M, T = p.T;
+__device__ __forceinline__ Best shfl_best(const Best &b, int o) {
+    return Best{__shfl_xor_sync(0xffffffffu, b.v, o), __shfl_xor_sync(0xffffffffu, b.z1, o),
+                __shfl_xor_sync(0xffffffffu, b.z2, o)};
+}
+
+// One CTA per window, one warp per model of the batch (blockDim = 32 * NM).
+// Eq. 13 init search: every (z1, z2) of the window -- real pairs are the window's
+// band entries (slot e of the alpha_3 layer), then (z1, eps), (eps, z2), (eps, eps) --
+// is scored for all NM models by all threads (each slot's NM values are one load of
+// the layer's state slot); block-wide lexicographic minimum per model.  Eq. 12
+// backtrack: warp k follows model k.
+template <int NM>
+__global__ void __launch_bounds__(256) k_backtrack(SceneView sc, const InstDesc *__restrict__ inst,
+                                                   const float *__restrict__ hist, int64_t L, BTArgs bt,
+                                                   DPParams p) {
+    __shared__ Best s_best[NM][8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
+    const InstDesc d = inst[blockIdx.x];
+    const int Sw = d.we - d.wb, M = bt.M, T = p.T, SS = bt.SS;
     const int EPSL = d.we;  // dummy label: orders after every real node (R11)
-    auto U = [&](int i, int n) { return __ldg(bt.U + ((int64_t)i * bt.nn + (n - bt.n_lo)) * NM + kk); };
+    auto Uk = [&](int i, int n, int k) { return __ldg(bt.U + ((int64_t)i * bt.nn + (n - bt.n_lo)) * NM + k); };
     auto layer = [&](int i) -> const float * {
         return (i >= 2 && i <= M - 1) ? hist + (int64_t)(i - 2) * L + d.off : nullptr;
     };
-    auto at = [&](const float *l, int s) { return l ? l[(int64_t)s * bt.SS + kk] : 0.f; };  // state stride SS
     // layer layout (dp_common.cuh): pair state (later, earlier) at qpad[earlier] - ppad + column
-    auto a_be = [&](const float *l, int b) { return at(l, d.ntail + (b - d.wb)); };
-    auto a_ea = [&](const float *l, int a) { return at(l, d.ntail + Sw + (a - d.wb)); };
-    auto a_ee = [&](const float *l) { return at(l, d.ntail + 2 * Sw); };
+    auto atk = [&](const float *l, int s, int k) { return l ? __ldg(l + (int64_t)s * SS + k) : 0.f; };
 
-    // ---- Eq. 13 init search
-    Best best{INFINITY, 0x7fffffff, 0x7fffffff};
+    // ---- Eq. 13 init search (all models at once)
+    Best best[NM];
+#pragma unroll
+    for (int k = 0; k < NM; ++k) best[k] = Best{INFINITY, 0x7fffffff, 0x7fffffff};
     if (M == 1) {
-        for (int c = d.wb + lane; c <= d.we; c += 32) {
-            const Best x{c < d.we ? __fmul_rn(p.l1, U(0, c)) : p.l1W, c, 0};
-            if (better(x, best)) best = x;
+        for (int c = d.wb + tid; c <= d.we; c += nthr) {
+#pragma unroll
+            for (int k = 0; k < NM; ++k) {
+                const Best x{c < d.we ? __fmul_rn(p.l1, Uk(0, c, k)) : p.l1W, c, 0};
+                if (better(x, best[k])) best[k] = x;
+            }
         }
     } else {
         const float *a3 = layer(2);
-        for (int z1 = d.wb + lane; z1 <= d.we; z1 += 32) {
-            const bool r1 = z1 < d.we;
-            const float u1 = r1 ? __fmul_rn(p.l1, U(0, z1)) : p.l1W;
-            int c0 = d.wb, c1 = d.we, q = 0, lo = 0;
-            if (r1) {
-                lo = sc.first(sc.t[z1] + 1);
-                c0 = lo;
-                c1 = min(sc.first(sc.t[z1] + T), d.we);
-                q = sc.qpad[z1];
+        const int npp = d.npp;
+        for (int q = tid; q < npp + 2 * Sw + 1; q += nthr) {
+            int z1 = EPSL, z2 = EPSL, slot;
+            bool ok = true;
+            if (q < npp) {  // real pair (z1 -> z2): band entry of row z1
+                z1 = __ldg(sc.prow_pad + d.ppad + q);
+                ok = z1 >= 0;
+                if (ok) {
+                    const int4 ni = __ldg(sc.ninfo + z1);  // (t', minnode(t'+1), qstart, qpad)
+                    z2 = ni.y + (d.ppad + q - ni.w);
+                    ok = z2 < d.we && __ldg(sc.t + z2) - ni.x < T;
+                }
+                slot = q;
+            } else if (q < npp + Sw) {  // (z1, eps): alpha_3(eps, z1) is the (eps, a) slot of z1
+                z1 = d.wb + (q - npp);
+                slot = d.ntail + Sw + (z1 - d.wb);
+            } else if (q < npp + 2 * Sw) {  // (eps, z2): alpha_3(z2, eps) is the (b, eps) slot of z2
+                z2 = d.wb + (q - npp - Sw);
+                slot = d.ntail + (z2 - d.wb);
+            } else {
+                slot = d.ntail + 2 * Sw;  // (eps, eps)
             }
-            for (int z2 = c0; z2 <= c1; ++z2) {
-                const bool r2 = z2 < c1;
-                const float u2 = r2 ? __fmul_rn(p.l1, U(1, z2)) : p.l1W;
-                float al;
-                if (r1 && r2) al = at(a3, q + (z2 - lo) - d.ppad);
-                else if (r1) al = a_ea(a3, z1);
-                else if (r2) al = a_be(a3, z2);
-                else al = a_ee(a3);
-                const Best x{__fadd_rn(__fadd_rn(u1, u2), al), z1, r2 ? z2 : EPSL};
-                if (better(x, best)) best = x;
+            if (!ok) continue;
+#pragma unroll
+            for (int k = 0; k < NM; ++k) {
+                const float u1 = z1 < EPSL ? __fmul_rn(p.l1, Uk(0, z1, k)) : p.l1W;
+                const float u2 = z2 < EPSL ? __fmul_rn(p.l1, Uk(1, z2, k)) : p.l1W;
+                const Best x{__fadd_rn(__fadd_rn(u1, u2), atk(a3, slot, k)), z1, z2};
+                if (better(x, best[k])) best[k] = x;
             }
         }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        Best y{__shfl_xor_sync(0xffffffffu, best.v, o), __shfl_xor_sync(0xffffffffu, best.z1, o),
-               __shfl_xor_sync(0xffffffffu, best.z2, o)};
-        if (better(y, best)) best = y;
+    for (int k = 0; k < NM; ++k) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const Best y = shfl_best(best[k], o);
+            if (better(y, best[k])) best[k] = y;
+        }
+        if (lane == 0) s_best[k][warp] = best[k];
     }
-    int za = best.z1, zb = best.z2;  // z1, z2 (EPSL = dummy)
+    __syncthreads();
+    if (warp >= NM) return;
+    const int kk = warp;  // this warp's model
+    Best bst = s_best[kk][0];
+    for (int w2 = 1; w2 < (nthr >> 5); ++w2)
+        if (better(s_best[kk][w2], bst)) bst = s_best[kk][w2];
+    auto U = [&](int i, int n) { return Uk(i, n, kk); };
+    auto at = [&](const float *l, int s) { return atk(l, s, kk); };
+    auto a_be = [&](const float *l, int b) { return at(l, d.ntail + (b - d.wb)); };
+    auto a_ea = [&](const float *l, int a) { return at(l, d.ntail + Sw + (a - d.wb)); };
+    auto a_ee = [&](const float *l) { return at(l, d.ntail + 2 * Sw); };
+    int za = bst.z1, zb = bst.z2;  // z1, z2 (EPSL = dummy)
     int64_t *zo = bt.z[kk] ? bt.z[kk] + (int64_t)d.out * M : nullptr;
     float A = za == EPSL ? p.W : U(0, za);
     if (lane == 0 && zo) zo[0] = za == EPSL ? -1 : sc.id[za];
@@ -132,14 +169,17 @@ __global__ void __launch_bounds__(128) k_backtrack_warp(SceneView sc, const Inst
             }
             return msg_n(a_be(nx, c), p.l1, U(i, c));
         };
+        // minimum and first argmin (ascending c), one value per lane and 32-candidate chunk
         float R = INFINITY;
-        for (int c = c0 + lane; c < c1; c += 32) R = fminf(R, value(c));
-        R = warp_min(R);
         int arg = -1;
-        for (int cb = c0; cb < c1 && arg < 0; cb += 32) {
+        for (int cb = c0; cb < c1; cb += 32) {
             const int c = cb + lane;
-            const unsigned hit = __ballot_sync(0xffffffffu, c < c1 && value(c) == R);
-            if (hit) arg = cb + __ffs(hit) - 1;
+            const float v = c < c1 ? value(c) : INFINITY;
+            const float cm = warp_min(v);
+            if (cm < R) {  // strictly better chunk: its first lane attaining cm
+                R = cm;
+                arg = cb + __ffs(__ballot_sync(0xffffffffu, c < c1 && v == cm)) - 1;
+            }
         }
         float eps;
         float real = R;
@@ -158,15 +198,29 @@ __global__ void __launch_bounds__(128) k_backtrack_warp(SceneView sc, const Inst
         zb = zc;
     }
     if (lane == 0) {
-        if (bt.E[kk]) bt.E[kk][d.out] = best.v;
+        if (bt.E[kk]) bt.E[kk][d.out] = bst.v;
         if (bt.A[kk]) bt.A[kk][d.out] = A;
     }
 }
 
 hgm_status launch_backtrack_warp(const SceneView &v, const InstDesc *dinst, int ninst, const float *hist, int64_t L,
                                  const BTArgs &bt, const DPParams &p, cudaStream_t s) {
-    const int npairs = ninst * bt.NM;
-    k_backtrack_warp<<<(npairs + 3) / 4, 128, 0, s>>>(v, dinst, npairs, hist, L, bt, p);
+    if (ninst <= 0) return HGM_OK;
+    const int threads = 32 * std::max(bt.NM, 4);  // >= 4 warps for the init search
+#define HGM_BT_CASE(n) \
+    case n: k_backtrack<n><<<ninst, threads, 0, s>>>(v, dinst, hist, L, bt, p); break
+    switch (bt.NM) {
+        HGM_BT_CASE(1);
+        HGM_BT_CASE(2);
+        HGM_BT_CASE(3);
+        HGM_BT_CASE(4);
+        HGM_BT_CASE(5);
+        HGM_BT_CASE(6);
+        HGM_BT_CASE(7);
+        HGM_BT_CASE(8);
+        default: return fail(HGM_ERR_INVALID_ARGUMENT, "model batch size must be 1..8");
+    }
+#undef HGM_BT_CASE
     return HGM_OK;
 }
 

@@ -448,10 +448,8 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
         const int4 *NI = reinterpret_cast<const int4 *>(sb + ly.ni);
         const float *EB = reinterpret_cast<const float *>(sb + ly.eb);
         const int *FTAB = reinterpret_cast<const int *>(sb + ly.ftab);
-        const int F0 = w.F0, F1 = w.F1, B0 = w.B0, B1 = w.B1, A0 = w.A0;
-        const int NR = B1 - A0, NBr = B1 - B0;
-        const int Sw = d.we - d.wb;
-        const int wend = d.o + caps.W;
+        const int B0 = w.B0, B1 = w.B1, A0 = w.A0;
+        const int NBr = B1 - B0;
         float *cur = hist + (int64_t)layer * L + d.off;
         auto first = [&](int f) { return f <= 0 ? 0 : (f > sc.fmax ? sc.S : FTAB[w.ft0 + (f - w.flo)]); };
         const unsigned char *bk = sb + ly.bk;  // the item's bookkeeping (k_item_prep)
@@ -464,7 +462,6 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
         const int *r_fc = r_qp + caps.NA;   // first / last coincident column
         const int *r_lc = r_fc + caps.NA;
         const uint8_t *smap = bk + bp.map;
-        (void)NR;
 
         // ---- messages: warps claim b rows; each row's entries become messages in place and
         // its (b, eps) state is finished; every finished row completes one tx unit of conv[s]
