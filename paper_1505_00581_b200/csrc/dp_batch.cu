@@ -88,10 +88,11 @@ struct BookPlan {
 // and become messages in place), its direction rows, the small raw inputs, its
 // bookkeeping record and the dummy terms of its b rows.  Byte offsets within the stage:
 struct StageLayout {
-    int en, th, uc, we, tc, ni, eb, ee, ftab, bk, bean, total;
+    int en, th, tb, uc, we, tc, ni, eb, ee, ftab, bk, bean, total;
     StageLayout() = default;
     // NE entries, NTH direction floats, NC candidate nodes, NA rows, NB b nodes, FT b-frames
     __host__ __device__ StageLayout(int NE, int NTH, int NC, int NA, int NB, int FT, int T, int NM, int book) {
+        // NE entries (and theta of the b rows), NTH direction floats of the a rows
         const int EPF = entry_floats(NM);
         int o = 0;
         auto take = [&](long long bytes) {
@@ -101,6 +102,7 @@ struct StageLayout {
         };
         en = take(4LL * EPF * NE);
         th = take(4LL * (NTH + 8));  // + 8: the copies widen ranges to whole 16-byte units
+        tb = take(4LL * (NE + 8));
         uc = take(4LL * (NM * NC + 8));
         we = take(4LL * (EPF * NC + 8));
         tc = take(4LL * (NC + 8));
@@ -115,7 +117,7 @@ struct StageLayout {
 };
 
 __host__ __device__ inline StageLayout item_layout(const WorkItem &w, int T, int NM, int book) {
-    return StageLayout(w.qb1 - w.qb0, w.qb1 - w.qa, w.Cend - w.B0, w.B1 - w.A0, w.B1 - w.B0, w.F1 - w.F0, T, NM, book);
+    return StageLayout(w.qb1 - w.qb0, w.qa1 - w.qa, w.Cend - w.B0, w.B1 - w.A0, w.B1 - w.B0, w.F1 - w.F0, T, NM, book);
 }
 
 // Shared memory: two stages of caps.STAGE bytes (the largest item layout of the call;
@@ -131,7 +133,7 @@ struct SmemPlan {
             return r;
         };
         stage[0] = take((size_t)c.STAGE);
-        stage[1] = take((size_t)c.STAGE);
+        stage[1] = c.NSTAGE > 1 ? take((size_t)c.STAGE) : stage[0];  // one stage: huge items (large T)
         fw = take(sizeof(float) * (size_t)NM * (c.FT + T));
         dl = take(sizeof(float) * (size_t)NM * T);
         ctl = take(1024);  // item descriptors and layouts, mbarriers, counters
@@ -309,7 +311,8 @@ __device__ __forceinline__ void issue_stage(const SceneView &sc, WorkItem &w, co
         w.ee0 = cl.range(sb + ly.ee, hist, nxo + (int64_t)(d.ntail + 2 * Sw) * EPF,
                          nxo + (int64_t)(d.ntail + 2 * Sw + 1) * EPF);
     }
-    w.th0 = w.qa - cl.range(sb + ly.th, sc.theta_pad, w.qa, w.qb1);  // TH[q] holds theta_pad[th0 + q]
+    w.th0 = w.qa - cl.range(sb + ly.th, sc.theta_pad, w.qa, w.qa1);  // TH[q] holds theta_pad[th0 + q]
+    w.tb0 = cl.range(sb + ly.tb, sc.theta_pad, w.qb0, w.qb1);         // theta(b -> c) of the b rows' entries
     w.uc0 = cl.range(sb + ly.uc, U, ui_off + (int64_t)w.B0 * NM, ui_off + (int64_t)w.Cend * NM);
     w.tc0 = cl.range(sb + ly.tc, sc.t, w.B0, w.Cend);
     if (w.B1 > w.A0) cl.raw(sb + ly.ni, sc.ninfo + w.A0, (unsigned)(sizeof(int4) * (w.B1 - w.A0)));
@@ -331,6 +334,7 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
     extern __shared__ __align__(128) unsigned char smem[];
     const SmemPlan sp(caps, p.T, NM);
     const BookPlan bp(caps, p.T);
+    const int nstage = caps.NSTAGE;  // 2 (double-buffered) or 1 (items too large for two)
     Ctl *ctl = reinterpret_cast<Ctl *>(smem + sp.ctl);
     float *DL = reinterpret_cast<float *>(smem + sp.dl);  // [T][NM] lambda2 |g_i - dt|
     float *fw = reinterpret_cast<float *>(smem + sp.fw);  // [FT + T][NM] frame minima of w
@@ -357,13 +361,13 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
         // flight while item m-1 still occupies the stage item m+1 will use
         int next_idx = lane == 0 ? atomicAdd(counter, 1) : 0;
         for (int m = 0;; ++m) {
-            const int st = m & 1;
+            const int st = m % nstage, use = m / nstage;  // use: how many items stage st held before
             WorkItem pre{};
             if (lane == 0) {
                 if (next_idx < nitems) pre = items[next_idx];
                 next_idx = next_idx < nitems ? atomicAdd(counter, 1) : nitems;
             }
-            if (m >= 2) mbar_wait(&ctl->free_[st], ((m - 2) >> 1) & 1, 1024);
+            if (use >= 1) mbar_wait(&ctl->free_[st], (use - 1) & 1, 1024);
             if (lane == 0) trace(m, 4);
             if (lane == 0) {
                 WorkItem &nw = ctl->w[st];
@@ -383,10 +387,11 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
                     mbar_arrive(&ctl->raw[st]);
                 }
             }
-            mbar_wait(&ctl->raw[st], (m >> 1) & 1);
+            mbar_wait(&ctl->raw[st], use & 1);
             if (lane == 0) trace(m, 6);
             const WorkItem &w = ctl->w[st];
             if (!w.live) break;
+            if (!w.primary) continue;  // another item of this b-tile finishes its dummy-form states
             const InstDesc &d = w.d;
             const StageLayout &ly = ctl->lay[st];
             const unsigned char *sb = smem + sp.stage[st];
@@ -431,9 +436,9 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
         return;
     }
     for (int m = 0;; ++m) {
-        const int s = m & 1;
+        const int s = m % nstage, use = m / nstage;
         if (tid == 0) trace(m, 0);
-        mbar_wait(&ctl->raw[s], (m >> 1) & 1);
+        mbar_wait(&ctl->raw[s], use & 1);
         if (tid == 0) trace(m, 1);
         const WorkItem &w = ctl->w[s];
         if (!w.live) break;
@@ -442,6 +447,7 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
         unsigned char *sb = smem + sp.stage[s];
         float *b_ean = reinterpret_cast<float *>(sb + ly.bean);  // [NB][NM] lambda1 W^d + alpha_{i+1}(eps, b)
         const float *TH = reinterpret_cast<const float *>(sb + ly.th);
+        const float *TB = reinterpret_cast<const float *>(sb + ly.tb);
         float *EN = reinterpret_cast<float *>(sb + ly.en);
         const float *UC = reinterpret_cast<const float *>(sb + ly.uc);
         const int *TC = reinterpret_cast<const int *>(sb + ly.tc);
@@ -474,7 +480,18 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
             const int4 ni = NI[r];
             const int tb = ni.x, c0 = ni.y;
             const int len = min(first(tb + T), d.we) - c0;  // candidates of row b in this window (R1, R2)
-            const int e0 = ni.w - w.qb0, t0 = ni.w - w.th0;
+            const int e0 = ni.w - w.qb0;
+#ifdef HGM_DEBUG_CHECKS
+            if (e0 < 0 || w.tb0 < 0 || w.tb0 > 3 || ly.total > caps.STAGE || e0 + len > w.qb1 - w.qb0 + 8 ||
+                c0 < B0 || c0 > w.Cend || tb < w.F0 || tb >= w.F1) {
+                if (lane == 0)
+                    printf("conv: blk %d item F[%d,%d) G[%d,%d) A0 %d B0 %d B1 %d rb %d r %d ni (%d,%d,%d,%d) qb0 %d qb1 %d "
+                           "tb0 %d prim %d len %d lay.total %d STAGE %d tb %d\n",
+                           blockIdx.x, w.F0, w.F1, w.G0, w.G1, A0, B0, B1, rb, r, ni.x, ni.y, ni.z, ni.w, w.qb0, w.qb1,
+                           w.tb0, w.primary, len, ly.total, caps.STAGE, ly.tb);
+                continue;
+            }
+#endif
             float mn[NM];
 #pragma unroll
             for (int k = 0; k < NM; ++k) mn[k] = INFINITY;
@@ -494,7 +511,7 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
                     mn[k] = fminf(mn[k], n);
                     ent[k] = __fadd_rn(n, dl[k]);  // msg_m
                 }
-                ent[NM] = TH[t0 + j];  // theta(b -> c)
+                ent[NM] = TB[w.tb0 + e];  // theta(b -> c)
 #pragma unroll
                 for (int k = NM + 1; k < EPF; ++k) ent[k] = 0.f;
 #pragma unroll
@@ -510,13 +527,13 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
             }
             if (lane < NM) {
                 const float ean = __fadd_rn(p.l1W, kHasNext ? EB[w.eb0 + rb * EPF + lane] : 0.f);
-                b_ean[rb * NM + lane] = ean;                                             // lambda1 W^d + alpha_{i+1}(eps, b)
-                cur[(int64_t)(d.ntail + B0 + rb - d.wb) * EPF + lane] = fminf(bm, ean);  // (b, eps)
+                b_ean[rb * NM + lane] = ean;  // lambda1 W^d + alpha_{i+1}(eps, b)
+                if (w.primary) cur[(int64_t)(d.ntail + B0 + rb - d.wb) * EPF + lane] = fminf(bm, ean);  // (b, eps)
             }
             __syncwarp();
             if (lane == 0) mbar_complete_tx(&ctl->conv[s], 1);
         }
-        mbar_wait(&ctl->conv[s], (m >> 1) & 1);  // all rows of the item are messages now
+        mbar_wait(&ctl->conv[s], use & 1);  // all rows of the item are messages now
         // ---- P3: real states.  A lane task is one b with a PAIR of a's of the same a-frame
         // (same candidate range), so each candidate entry (b, c_j) is loaded once for two
         // states; warps claim 32-task groups (gap-major order: longest trips first).
@@ -644,31 +661,43 @@ __global__ void k_init_ee(const InstDesc *__restrict__ inst, int ninst, float *_
     hist[(int64_t)layer * L + d.off + (int64_t)(d.ntail + 2 * (d.we - d.wb)) * entry_floats(NM) + m] = INFINITY;
 }
 
-// Work items of a chunk, one thread per window: the global tiles meeting the
-// window's frames, clipped to them, at item_base[k] ...; descriptors are valid for
-// every step of the chunk.
+// Work items of a chunk, one thread per window: for every global b-tile meeting the
+// window's frames, its a-frame chunks (one chunk unless T is large) that meet them,
+// clipped; the first item of each b-tile is its "primary".  Written at
+// item_base[k] - base0 ...; descriptors are valid for every step of the chunk.
 __global__ void k_items(SceneView sc, const InstDesc *__restrict__ inst, int ninst, int W, int T,
                         const int32_t *__restrict__ gstart, const int32_t *__restrict__ tile_of, int tf_lo,
+                        const int32_t *__restrict__ sub_begin, const int32_t *__restrict__ sub_g,
                         const int32_t *__restrict__ item_base, int base0, WorkItem *items) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= ninst) return;
     const InstDesc d = inst[k];
-    const int g0 = __ldg(tile_of + (d.o - tf_lo)), n = __ldg(item_base + k + 1) - __ldg(item_base + k);
-    for (int x = 0; x < n; ++x) {
-        WorkItem w{};
-        w.d = d;
-        w.live = 1;
-        w.idx = __ldg(item_base + k) - base0 + x;
-        w.F0 = max(__ldg(gstart + g0 + x), d.o);
-        w.F1 = min(__ldg(gstart + g0 + x + 1), d.o + W);
-        w.B0 = sc.first(w.F0);
-        w.B1 = sc.first(w.F1);
-        w.A0 = max(sc.first(w.F0 - T + 1), d.wb);
-        w.Cend = min(sc.first(w.F1 + T - 1), d.we);
-        w.qa = __ldg(sc.qpad + w.A0);
-        w.qb0 = __ldg(sc.qpad + w.B0);
-        w.qb1 = __ldg(sc.qpad + w.B1);
-        items[w.idx] = w;
+    const int g_first = __ldg(tile_of + (d.o - tf_lo)), g_last = __ldg(tile_of + (d.o + W - 1 - tf_lo));
+    int idx = __ldg(item_base + k) - base0;
+    for (int gt = g_first; gt <= g_last; ++gt) {
+        bool first_of_tile = true;
+        for (int sb = __ldg(sub_begin + gt); sb < __ldg(sub_begin + gt + 1); ++sb) {
+            WorkItem w{};
+            w.d = d;
+            w.live = 1;
+            w.F0 = max(__ldg(gstart + gt), d.o);
+            w.F1 = min(__ldg(gstart + gt + 1), d.o + W);
+            w.G0 = max(__ldg(sub_g + 2 * sb), d.o);
+            w.G1 = min(__ldg(sub_g + 2 * sb + 1), w.F1);
+            if (w.G0 >= w.G1 && !first_of_tile) continue;  // chunk entirely before the window
+            w.primary = first_of_tile ? 1 : 0;
+            first_of_tile = false;
+            w.idx = idx;
+            w.B0 = sc.first(w.F0);
+            w.B1 = sc.first(w.F1);
+            w.A0 = max(sc.first(w.G0), d.wb);
+            w.Cend = min(sc.first(w.F1 + T - 1), d.we);
+            w.qa = __ldg(sc.qpad + w.A0);
+            w.qa1 = __ldg(sc.qpad + max(sc.first(w.G1), w.A0));
+            w.qb0 = __ldg(sc.qpad + w.B0);
+            w.qb1 = __ldg(sc.qpad + w.B1);
+            items[idx++] = w;
+        }
     }
 }
 
@@ -705,7 +734,7 @@ __global__ void __launch_bounds__(256) k_item_prep(SceneView sc, const WorkItem 
     if (tid < nseg) {  // segments, gap-major: long candidate ranges first
         const int g = 1 + tid / (F1 - F0);
         const int f = F0 + tid % (F1 - F0);
-        if (f - g >= w.d.o) {
+        if (f - g >= w.d.o && f - g >= w.G0 && f - g < w.G1) {
             sg.g = g;
             sg.b0 = sc.first(f);
             sg.nb = sc.first(f + 1) - sg.b0;
@@ -823,11 +852,11 @@ hgm_status launch_dp_batch(int NM, const SceneView &v, const WorkItem *items, in
 }
 
 hgm_status launch_items(const SceneView &v, const InstDesc *dinst, int ninst, int W, int T, const int32_t *gstart,
-                        const int32_t *tile_of, int tf_lo, const int32_t *item_base, int base0, WorkItem *items,
-                        cudaStream_t s) {
+                        const int32_t *tile_of, int tf_lo, const int32_t *sub_begin, const int32_t *sub_g,
+                        const int32_t *item_base, int base0, WorkItem *items, cudaStream_t s) {
     if (ninst > 0)
-        k_items<<<(ninst + 127) / 128, 128, 0, s>>>(v, dinst, ninst, W, T, gstart, tile_of, tf_lo, item_base, base0,
-                                                    items);
+        k_items<<<(ninst + 127) / 128, 128, 0, s>>>(v, dinst, ninst, W, T, gstart, tile_of, tf_lo, sub_begin, sub_g,
+                                                    item_base, base0, items);
     return HGM_OK;
 }
 

@@ -69,6 +69,7 @@ struct TileCaps {  // shared-memory capacities of one K-DP work item, maxima ove
     int FT;     // b-frames
     int W;      // window length in frames
     int STAGE;  // bytes of one K-DP shared-memory stage (largest item layout)
+    int NSTAGE; // stages: 2 (the next item streams in while one is processed) or 1 (huge items)
 };
 
 // One K-DP work item: a tile of b-frames [F0, F1) of one window (dp_batch.cu).
@@ -81,8 +82,11 @@ struct WorkItem {
     int A0;        // first direction row: max(minnode(F0 - T + 1), window start)
     int Cend;      // candidate nodes end: min(minnode(F1 + T - 1), window end)
     int qa, qb0, qb1;  // qpad[A0], qpad[B0], qpad[B1]
+    int G0, G1;    // a-frames [G0, G1) of the item's real states (the whole range unless T is large)
+    int qa1;       // qpad[minnode(G1)]: end of the direction rows the loop reads
+    int primary;   // 1: this item also finishes the b rows' dummy-form states (one item per b-tile)
     // filled by the producer lane: shared-memory index of each range's first element
-    int th0, we0, eb0, ee0, uc0, tc0, rf0, ft0, flo;
+    int th0, tb0, we0, eb0, ee0, uc0, tc0, rf0, ft0, flo;
 };
 
 constexpr int MAX_BATCH = 8;  // models of equal M evaluated together by one CTA

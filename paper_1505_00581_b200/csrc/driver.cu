@@ -3,6 +3,7 @@
 // alpha history, one K-DP launch per recursion step i = M..3 (Eq. 10, the
 // paper's host loop of Alg. 2 with the whole batch of windows per launch), then K-BT.
 #include <algorithm>
+#include <cstdio>
 #include <memory>
 #include <cstdlib>
 #include <cstring>
@@ -20,8 +21,8 @@ hgm_status launch_dp_batch(int NM, const SceneView &v, const WorkItem *items, in
                            const StepConstB &kc, const float *U, int64_t ui_off, const DPParams &p,
                            const TileCaps &caps, cudaStream_t s);
 hgm_status launch_items(const SceneView &v, const InstDesc *dinst, int ninst, int W, int T, const int32_t *gstart,
-                        const int32_t *tile_of, int tf_lo, const int32_t *item_base, int base0, WorkItem *items,
-                        cudaStream_t s);
+                        const int32_t *tile_of, int tf_lo, const int32_t *sub_begin, const int32_t *sub_g,
+                        const int32_t *item_base, int base0, WorkItem *items, cudaStream_t s);
 hgm_status launch_init_ee(const InstDesc *dinst, int ninst, float *hist, int64_t L, int layer, int NM,
                           cudaStream_t s);
 size_t dp_batch_smem(const TileCaps &c, int T, int NM);
@@ -105,9 +106,26 @@ bool use_v0_kernels() {
 // plan fits the budget (2 CTAs per SM), else a 1-CTA-per-SM budget is tried.
 struct Tiling {
     TileCaps caps{};
-    std::vector<int32_t> gstart;   // tile start frames, then f_hi, then sentinels
-    std::vector<int32_t> tile_of;  // tile index of frame f_lo + q
-    int f_lo = 0, slots = 1;
+    std::vector<int32_t> gstart;     // b-tile start frames, then f_hi, then sentinels
+    std::vector<int32_t> tile_of;    // b-tile index of frame f_lo + q
+    std::vector<int32_t> sub_begin;  // a-frame chunks of b-tile q: [sub_begin[q], sub_begin[q+1])
+    std::vector<int32_t> sub_g;      // chunk j covers a-frames [sub_g[2j], sub_g[2j+1])
+    int f_lo = 0;
+    // work items of the window starting at frame `of` (the same rule as k_items)
+    int items_of(int64_t of, int W) const {
+        int n = 0;
+        for (int gt = tile_of[of - f_lo]; gt <= tile_of[of + W - 1 - f_lo]; ++gt) {
+            const int64_t F1 = std::min<int64_t>(gstart[gt + 1], of + W);
+            bool first = true;
+            for (int sb = sub_begin[gt]; sb < sub_begin[gt + 1]; ++sb) {
+                const int64_t G0 = std::max<int64_t>(sub_g[2 * sb], of), G1 = std::min<int64_t>(sub_g[2 * sb + 1], F1);
+                if (G0 >= G1 && !first) continue;
+                first = false;
+                ++n;
+            }
+        }
+        return n;
+    }
 };
 
 static bool make_tiling(const hgm_scene *sc, const hgm_offsets &o, int T, int NM, Tiling *tl) {
@@ -117,57 +135,79 @@ static bool make_tiling(const hgm_scene *sc, const hgm_offsets &o, int T, int NM
     auto NF = [&](int64_t f) { return (int64_t)host_first(sc, f); };
     const int FT_max = std::max(1, std::min(8, 255 / std::max(1, T - 1)));
     const char *benv = getenv("HGM_SMEM_KB");  // tuning knob: shared memory per CTA (2 CTAs per SM by default)
-    const size_t budgets[2] = {(size_t)(benv ? atoi(benv) : 110) * 1024, 220 * 1024};
-    auto foot = [&](int64_t a, int64_t b, int64_t book) {  // stage bytes of the unclipped tile [a, b)
-        return (int64_t)item_stage_bytes((int)(QP(b) - QP(a)), (int)(QP(b) - QP(a - T + 1)), (int)(NF(b + T - 1) - NF(a)),
-                                         (int)(NF(b) - NF(a - T + 1)), (int)(NF(b) - NF(a)), (int)(b - a), T, NM,
-                                         (int)book);
+    // (shared-memory budget, stages): 2 CTAs/SM double-buffered; 1 CTA/SM double-buffered;
+    // 1 CTA/SM single stage (items too large for two, i.e. large T)
+    const size_t budgets[3] = {(size_t)(benv ? atoi(benv) : 110) * 1024, 220 * 1024, 220 * 1024};
+    const int stages[3] = {2, 2, 1};
+    // stage bytes of the unclipped item: b-frames [a, b), a-frames [g0, g1)
+    auto foot = [&](int64_t a, int64_t b, int64_t g0, int64_t g1, int64_t book) {
+        return (int64_t)item_stage_bytes((int)(QP(b) - QP(a)), (int)(QP(g1) - QP(g0)), (int)(NF(b + T - 1) - NF(a)),
+                                         (int)(NF(b) - NF(g0)), (int)(NF(b) - NF(a)), (int)(b - a), T, NM, (int)book);
     };
-    for (int bi = 0; bi < 2; ++bi) {
-        TileCaps c0{1, 1, 1, 1, 1, 1, FT_max, o.window, 0};
-        const int64_t fixed = (int64_t)dp_batch_smem(c0, T, NM);  // stage-independent part
-        const int64_t cap = ((int64_t)budgets[bi] - fixed) / 2 / 16 * 16;
-        int64_t book = (int64_t)item_book_bytes(c0, T);
-        for (int iter = 0; iter < 4; ++iter) {
+    for (int bi = 0; bi < 3; ++bi) {
+        TileCaps c0{1, 1, 1, 1, 1, 1, FT_max, o.window, 0, stages[bi]};
+        const int64_t fixed = (int64_t)dp_batch_smem(c0, T, NM);  // stage-independent part (upper bound)
+        const int64_t cap = ((int64_t)budgets[bi] - fixed) / stages[bi] / 16 * 16;
+        TileCaps cb{1, 1, 1, 1, 1, 1, 1, o.window, 0, stages[bi]};
+        int64_t book = (int64_t)item_book_bytes(cb, T);  // grows below until it covers the tiles made with it
+        for (int iter = 0; iter < 6; ++iter) {
             Tiling t;
             t.f_lo = (int)f_lo;
-            TileCaps c{1, 1, 1, 1, 1, 1, 1, o.window, 0};
-            for (int64_t F0 = f_lo; F0 < f_hi;) {
-                int64_t F1 = F0 + 1;  // a single frame is always a tile
-                while (F1 < f_hi && F1 - F0 < FT_max && foot(F0, F1 + 1, book) <= cap) ++F1;
-                t.gstart.push_back((int32_t)F0);
-                c.STAGE = (int)std::max<int64_t>(c.STAGE, foot(F0, F1, book));
+            TileCaps c{1, 1, 1, 1, 1, 1, 1, o.window, 0, stages[bi]};
+            bool fits = true;
+            auto account = [&](int64_t F0, int64_t F1, int64_t G0, int64_t G1) {
+                c.STAGE = (int)std::max<int64_t>(c.STAGE, foot(F0, F1, G0, G1, book));
                 c.NE = (int)std::max<int64_t>(c.NE, QP(F1) - QP(F0));
-                c.TH = (int)std::max<int64_t>(c.TH, QP(F1) - QP(F0 - T + 1) + 8);
-                c.NA = (int)std::max<int64_t>(c.NA, NF(F1) - NF(F0 - T + 1));
+                c.TH = (int)std::max<int64_t>(c.TH, QP(G1) - QP(G0) + 8);
+                c.NA = (int)std::max<int64_t>(c.NA, NF(F1) - NF(G0));
                 c.NB = (int)std::max<int64_t>(c.NB, NF(F1) - NF(F0));
                 c.NC = (int)std::max<int64_t>(c.NC, NF(F1 + T - 1) - NF(F0));
                 int64_t nst = 0;
-                for (int64_t f = F0; f < F1; ++f) nst += (NF(f + 1) - NF(f)) * (NF(f) - NF(f - T + 1));
+                for (int64_t f = F0; f < F1; ++f)
+                    nst += (NF(f + 1) - NF(f)) * (NF(std::min(f, G1)) - NF(std::max(f - T + 1, G0)));
                 c.NST = (int)std::max<int64_t>(c.NST, nst);
                 c.FT = (int)std::max<int64_t>(c.FT, F1 - F0);
+                t.sub_g.push_back((int32_t)G0);
+                t.sub_g.push_back((int32_t)G1);
+            };
+            for (int64_t F0 = f_lo; F0 < f_hi && fits;) {
+                int64_t F1 = F0 + 1;  // a single frame is always a b-tile
+                while (F1 < f_hi && F1 - F0 < FT_max && foot(F0, F1 + 1, F0 - T + 1, F1 + 1, book) <= cap) ++F1;
+                t.gstart.push_back((int32_t)F0);
+                t.sub_begin.push_back((int32_t)(t.sub_g.size() / 2));
+                if (foot(F0, F1, F0 - T + 1, F1, book) <= cap) {
+                    account(F0, F1, F0 - T + 1, F1);  // one item covers every a-frame
+                } else {  // large T (only a single b-frame gets here): its a-frames [F0 - T + 1, F1) in chunks
+                    for (int64_t G0 = F0 - T + 1; G0 < F1 && fits;) {
+                        int64_t G1 = G0 + 1;
+                        if (foot(F0, F1, G0, G1, book) > cap) fits = false;
+                        while (G1 < F1 && foot(F0, F1, G0, G1 + 1, book) <= cap) ++G1;
+                        account(F0, F1, G0, G1);
+                        G0 = G1;
+                    }
+                }
                 F0 = F1;
             }
-            c.FT = FT_max;  // the copy warp's frame-minima buffer is sized for FT_max
+            if (!fits) break;  // a single (b-frame, a-frame) item exceeds this budget
             const int64_t need_book = (int64_t)item_book_bytes(c, T);
             if (need_book > book) {  // the bookkeeping record grew: retile with it
                 book = need_book;
                 continue;
             }
-            if (c.STAGE > cap || dp_batch_smem(c, T, NM) > budgets[bi]) break;  // a single frame exceeds this budget
+            if (c.STAGE > cap || dp_batch_smem(c, T, NM) > budgets[bi]) break;
             const int ntiles = (int)t.gstart.size();
             t.gstart.push_back((int32_t)f_hi);
+            t.sub_begin.push_back((int32_t)(t.sub_g.size() / 2));
             t.tile_of.resize((size_t)(f_hi - f_lo));
             for (int q = 0; q < ntiles; ++q)
                 for (int64_t f = t.gstart[q]; f < t.gstart[q + 1]; ++f) t.tile_of[f - f_lo] = q;
-            int slots = 1;
-            for (int k = 0; k < o.count; ++k) {
-                const int64_t of = (int64_t)o.first_frame + (int64_t)k * o.stride;
-                slots = std::max(slots, t.tile_of[of + o.window - 1 - f_lo] - t.tile_of[of - f_lo] + 1);
-            }
-            for (int q = 0; q <= slots; ++q) t.gstart.push_back(INT32_MAX / 2);
-            t.slots = slots;
+            t.gstart.push_back(INT32_MAX / 2);
+            t.sub_begin.push_back(t.sub_begin.back());
             c.STAGE = (int)std::max<int64_t>(c.STAGE, 16);
+            if (getenv("HGM_DEBUG_TILING"))  // diagnosis
+                fprintf(stderr, "tiling: budget %zu cap %lld tiles %d subs %zu STAGE %d NE %d TH %d NA %d NB %d NC %d NST %d smem %zu\n",
+                        budgets[bi], (long long)cap, ntiles, t.sub_g.size() / 2, c.STAGE, c.NE, c.TH, c.NA, c.NB, c.NC,
+                        c.NST, dp_batch_smem(c, T, NM));
             t.caps = c;
             *tl = std::move(t);
             return true;
@@ -204,8 +244,14 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
     Tiling tl;
     if (!v0 && !make_tiling(sc, o, pp.T, NM, &tl))
         return fail(HGM_ERR_INVALID_ARGUMENT, "frames too dense for the shared-memory tile (reduce T or window)");
-    DevBuf d_gstart, d_tile_of;
+    DevBuf d_gstart, d_tile_of, d_subb, d_subg;
     if (!v0) {
+        HGM_TRY(d_subb.alloc(sizeof(int32_t) * tl.sub_begin.size(), s));
+        HGM_TRY(d_subg.alloc(sizeof(int32_t) * std::max<size_t>(2, tl.sub_g.size()), s));
+        HGM_CUDA(cudaMemcpyAsync(d_subb.p, tl.sub_begin.data(), sizeof(int32_t) * tl.sub_begin.size(),
+                                 cudaMemcpyHostToDevice, s));
+        HGM_CUDA(cudaMemcpyAsync(d_subg.p, tl.sub_g.data(), sizeof(int32_t) * tl.sub_g.size(), cudaMemcpyHostToDevice,
+                                 s));
         HGM_TRY(d_gstart.alloc(sizeof(int32_t) * tl.gstart.size(), s));
         HGM_TRY(d_tile_of.alloc(sizeof(int32_t) * std::max<size_t>(1, tl.tile_of.size()), s));
         HGM_CUDA(cudaMemcpyAsync(d_gstart.p, tl.gstart.data(), sizeof(int32_t) * tl.gstart.size(),
@@ -278,10 +324,7 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
             d.off = c.L;
             c.L += ns * SS;
             c.maxNs = std::max(c.maxNs, ns);
-            if (!v0) {
-                const int of = d.o;
-                ibase_all[c.k1 + 1] = ibase_all[c.k1] + tl.tile_of[of + o.window - 1 - tl.f_lo] - tl.tile_of[of - tl.f_lo] + 1;
-            }
+            if (!v0) ibase_all[c.k1 + 1] = ibase_all[c.k1] + tl.items_of(d.o, o.window);
             ++c.k1;
         }
         c.nitems = ibase_all[c.k1] - ibase_all[k0];
@@ -357,7 +400,8 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
             }
             HGM_CUDA(cudaMemsetAsync(counters_p, 0, sizeof(int) * nsteps, ls));
             launch_items(v, di, ninst, o.window, p.T, d_gstart.as<int32_t>(), d_tile_of.as<int32_t>(), tl.f_lo,
-                         d_ibase.as<int32_t>() + k0, ibase_all[k0], items_p, ls);
+                         d_subb.as<int32_t>(), d_subg.as<int32_t>(), d_ibase.as<int32_t>() + k0, ibase_all[k0], items_p,
+                         ls);
             launch_item_prep(v, items_p, nitems, tl.caps, p.T, book_p, ls);
             launch_init_ee(di, ninst, hist, L, nsteps - 1, NM, ls);  // first layer's (eps, eps) slots
             count_launch(K_DP, 3);
