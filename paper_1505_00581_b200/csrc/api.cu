@@ -408,7 +408,7 @@ hgm_status hgm_detect_actions(const hgm_model *const *models, int32_t n_models, 
     float *Ed = dEall ? E_all : Eb.as<float>();
     HGM_TRY(zb.alloc(sizeof(int64_t) * (size_t)count * Mmax * MAX_BATCH_API, s));
     // batches of consecutive models with equal chain length share one K-DP pass
-    const int max_batch = use_v0_kernels() ? 1 : MAX_BATCH_API;
+    int max_batch = use_v0_kernels() ? 1 : MAX_BATCH_API;
     for (int m0 = 0; m0 < n_models;) {
         int m1 = m0 + 1;
         while (m1 < n_models && m1 - m0 < max_batch && models[m1]->M == models[m0]->M) ++m1;
@@ -423,7 +423,14 @@ hgm_status hgm_detect_actions(const hgm_model *const *models, int32_t n_models, 
         for (int k = 0; k < NM; ++k)
             mo[k] = MatchOut{Ed + (size_t)(m0 + k) * count, Ab.as<float>() + (size_t)(m0 + k) * count,
                              zb.as<int64_t>() + (size_t)k * count * Mmax};
-        HGM_TRY(match_batch(models + m0, NM, scene, *params, *offsets, U.as<float>(), n_lo, nn, mo, s));
+        g_tiling_failed = false;
+        const hgm_status bst = match_batch(models + m0, NM, scene, *params, *offsets, U.as<float>(), n_lo, nn, mo, s);
+        if (bst != HGM_OK && g_tiling_failed && NM > 1) {
+            max_batch = 1;  // too dense for a batch's stage: one model at a time from here on
+            m1 = m0;
+            continue;
+        }
+        HGM_TRY(bst);
         m0 = m1;
     }
     scene->uses.record(s);

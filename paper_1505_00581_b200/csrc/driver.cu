@@ -92,6 +92,8 @@ static ScratchSet &scratch_set(int device) {
     return *sets[d];
 }
 
+thread_local bool g_tiling_failed = false;
+
 bool use_v0_kernels() {
     const char *e = getenv("HGM_KERNEL");
     return e && strcmp(e, "v0") == 0;
@@ -224,8 +226,19 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
     const int count = o.count, M = models[0]->M;
     if (count <= 0) return HGM_OK;
     if (NM < 1 || NM > MAX_BATCH) return fail(HGM_ERR_INVALID_ARGUMENT, "model batch size must be 1..8");
-    const bool v0 = use_v0_kernels();
+    bool v0 = use_v0_kernels();
     if (v0 && NM != 1) return fail(HGM_ERR_INVALID_ARGUMENT, "v0 kernels take one model at a time");
+    Tiling tl;
+    if (!v0 && !make_tiling(sc, o, pp.T, NM, &tl)) {
+        // a single (b-frame, a-frame) item of these frames exceeds shared memory (very
+        // dense frames at large T): a batch is retried one model at a time by the caller,
+        // and a single model falls back to the reference kernels (global-memory operands)
+        if (NM > 1) {
+            g_tiling_failed = true;
+            return fail(HGM_ERR_INVALID_ARGUMENT, "frames too dense for the shared-memory tile of a model batch");
+        }
+        v0 = true;
+    }
     std::vector<InstDesc> all(count);
     for (int k = 0; k < count; ++k) {
         const int64_t of = (int64_t)o.first_frame + (int64_t)k * o.stride;
@@ -241,9 +254,6 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
         d.o = (int32_t)of;
         all[k] = d;
     }
-    Tiling tl;
-    if (!v0 && !make_tiling(sc, o, pp.T, NM, &tl))
-        return fail(HGM_ERR_INVALID_ARGUMENT, "frames too dense for the shared-memory tile (reduce T or window)");
     DevBuf d_gstart, d_tile_of, d_subb, d_subg;
     if (!v0) {
         HGM_TRY(d_subb.alloc(sizeof(int32_t) * tl.sub_begin.size(), s));

@@ -135,6 +135,7 @@ struct MatchOut {  // per (model, offset) results of one model
     int64_t *z;     // [count * M] device
 };
 bool use_v0_kernels();
+extern thread_local bool g_tiling_failed;  // set by match_batch when a model batch must be split
 hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *sc, const hgm_params &pp,
                        const hgm_offsets &o, const float *U, int64_t n_lo, int64_t nn, const MatchOut *outs,
                        cudaStream_t s);

@@ -220,7 +220,9 @@ def test_tiled_kernel_bitexact_to_reference_kernel(hgm, name, kw, monkeypatch):
         assert torch.equal(a.E, b.E) and torch.equal(a.A, b.A) and torch.equal(a.z, b.z)
 
 
-@pytest.mark.parametrize("name,kw", [("C2", {}), ("C3", dict(n_frames=2000)), ("C4", dict(T=10, n_frames=900))])
+@pytest.mark.parametrize("name,kw", [("C2", {}), ("C3", dict(n_frames=2000)), ("C4", dict(T=10, n_frames=900)),
+                                     ("C4", dict(T=20, n_frames=460)), ("C4", dict(T=40, n_frames=450)),
+                                     ("C4", dict(T=80, n_frames=420))])
 def test_model_batched_kernel_bitexact(hgm, name, kw, monkeypatch):
     """detect_actions batches the 6 models of equal M into one K-DP pass; the
     per-model reference kernels (HGM_KERNEL=v0) must give identical bits."""
@@ -243,8 +245,10 @@ def test_model_batched_kernel_bitexact(hgm, name, kw, monkeypatch):
         assert torch.equal(a.E_all, b.E_all) and torch.equal(a.winner, b.winner) and torch.equal(a.score, b.score)
 
 
-@pytest.mark.parametrize("ft", [1, 3, 8])
-def test_tile_sizes_bitexact(hgm, ft, monkeypatch):
+@pytest.mark.parametrize("smem_kb", [20, 32, 48, 110])
+def test_tile_sizes_bitexact(hgm, smem_kb, monkeypatch):
+    """Shared-memory budgets from tiny (one-frame tiles whose a-frames are split into
+    chunks, single-stage items) to the default: every tiling gives the v0 bits."""
     import torch
 
     wl = synth.make_workload("C1")
@@ -254,7 +258,7 @@ def test_tile_sizes_bitexact(hgm, ft, monkeypatch):
     monkeypatch.setenv("HGM_KERNEL", "v0")
     a = hgm.match_model_at_offsets(m, s, p, 0, 1, 541, 60)
     monkeypatch.setenv("HGM_KERNEL", "v1")
-    monkeypatch.setenv("HGM_TILE_FRAMES", str(ft))
+    monkeypatch.setenv("HGM_SMEM_KB", str(smem_kb))
     b = hgm.match_model_at_offsets(m, s, p, 0, 1, 541, 60)
     torch.cuda.synchronize()
     assert torch.equal(a.E, b.E) and torch.equal(a.z, b.z)
