@@ -261,6 +261,7 @@ def main():
     for w_ in range(args.warmup):
         if w_ == args.warmup - 1:
             hgm.set_profiling(True)  # the last warm-up step already runs with the event timers on
+        flush.zero_()  # (first launch of torch's fill kernel loads its module lazily: not in the timed region)
         step()
     torch.cuda.synchronize()
     hgm.set_profiling(True)
