@@ -602,17 +602,16 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
                         R1[k] = fminf(R1[k], v1[k]);
                     }
                 }
-            } else {  // exact flag-aware loop (coincident points, R10)
-                const int qb = r_q[rbt];
-                const int qa0 = r_q[ra0], qa1 = r_q[ra1];
-                const bool co_ab0 = live && __ldg(sc.coinc + qa0 + colb);
-                const bool co_ab1 = live && __ldg(sc.coinc + qa1 + colb);
+            } else {  // exact flag-aware loop (coincident points, R10): the padded band holds NaN
+                      // for the direction of a zero-length ray, so the flags come with the angles
+                const bool co_ab0 = live && isnan(th_ab0);
+                const bool co_ab1 = live && isnan(th_ab1);
                 for (int j = 0; j < trip; ++j) {
                     float e0[EPF];
                     ld_entry<EPF>(erow + (size_t)j * EPF, e0);
-                    const bool cbc = __ldg(sc.coinc + qb + j);
-                    const bool cac0 = __ldg(sc.coinc + qa0 + sg.aoff + j);
-                    const bool cac1 = __ldg(sc.coinc + qa1 + sg.aoff + j);
+                    const bool cbc = isnan(e0[NM]);
+                    const bool cac0 = isnan(arow0[j]);
+                    const bool cac1 = isnan(arow1[j]);
 #pragma unroll
                     for (int k = 0; k < NM; ++k) {
                         R0[k] = fminf(R0[k], cand_value(e0[k], e0[NM], th_ab0, arow0[j], cbc || co_ab0, cbc || cac0,

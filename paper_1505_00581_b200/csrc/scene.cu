@@ -4,7 +4,9 @@
 // minnode table first_tab[f] = first node with frame >= f (R4), and the pair
 // band: for every node a, its successors c in frames (t'(a), t'(a) + T_max),
 // which are the contiguous node range [minnode(t'(a)+1), minnode(t'(a)+T_max)).
-// The band stores the ray direction theta(a->c) (K-G) and a coincidence flag.
+// The band stores the ray direction theta(a->c) (K-G) and a coincidence flag; the
+// padded copy K-DP stages (theta_pad) holds NaN instead of the direction of a
+// zero-length ray, so the flag travels with the angle.
 // Every admissible DP state (b, a) is one band entry, and every
 // per-candidate operand of the recursion is a band entry too.
 //
@@ -92,7 +94,7 @@ __global__ void k_band(int64_t S, int T_max, int fmax, const int32_t *__restrict
         const bool co = ax == cx && ay == cy;
         const float th = dir_of(ax, ay, cx, cy);
         theta[p] = th;
-        tp[c - lo] = th;
+        tp[c - lo] = co ? __int_as_float(0x7fc00000) : th;  // K-DP's copy: NaN marks a zero-length ray (R10)
         rp[c - lo] = (int32_t)a;
         coinc[p] = co ? 1 : 0;
         run += co ? 1u : 0u;
