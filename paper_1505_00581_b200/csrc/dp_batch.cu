@@ -124,7 +124,7 @@ __host__ __device__ inline StageLayout item_layout(const WorkItem &w, int T, int
 // while one item is processed the copies of the next one land in the other stage),
 // the copy warp's frame minima, the Delta table and the control block.
 struct SmemPlan {
-    size_t stage[2], fw, dl, ctl, total;
+    size_t stage[3], fw, dl, ctl, total;
     __host__ __device__ SmemPlan(const TileCaps &c, int T, int NM) {
         size_t o = 0;
         auto take = [&](size_t bytes) {
@@ -134,6 +134,7 @@ struct SmemPlan {
         };
         stage[0] = take((size_t)c.STAGE);
         stage[1] = c.NSTAGE > 1 ? take((size_t)c.STAGE) : stage[0];  // one stage: huge items (large T)
+        stage[2] = c.NSTAGE > 2 ? take((size_t)c.STAGE) : stage[0];
         fw = take(sizeof(float) * (size_t)NM * (c.FT + T));
         dl = take(sizeof(float) * (size_t)NM * T);
         ctl = take(1024);  // item descriptors and layouts, mbarriers, counters
@@ -273,13 +274,13 @@ __device__ __forceinline__ void trace(int m, int ev) {
 
 // Control block in shared memory.
 struct Ctl {
-    WorkItem w[2];      // stage descriptors (w[s].live == 0: no more items)
-    StageLayout lay[2]; // stage layouts
-    int row_claim[2];   // next unconverted b row of the stage's item
-    int task_claim[2];  // next unclaimed 32-task group
-    uint64_t raw[2];    // stage inputs landed (copy-warp arrival + TMA bytes)
-    uint64_t conv[2];   // every b row converted (one tx unit per row)
-    uint64_t free_[2];  // stage released: one arrival per compute warp
+    WorkItem w[3];      // stage descriptors (w[s].live == 0: no more items)
+    StageLayout lay[3]; // stage layouts
+    int row_claim[3];   // next unconverted b row of the stage's item
+    int task_claim[3];  // next unclaimed 32-task group
+    uint64_t raw[3];    // stage inputs landed (copy-warp arrival + TMA bytes)
+    uint64_t conv[3];   // every b row converted (one tx unit per row)
+    uint64_t free_[3];  // stage released: one arrival per compute warp
 };
 
 __device__ __forceinline__ void mbar_complete_tx(uint64_t *bar, unsigned n) {
@@ -346,7 +347,7 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
         DL[q] = delta_term(p.l2, kc.c[k].x, dt);
     }
     if (tid == 0) {
-        for (int st = 0; st < 2; ++st) {
+        for (int st = 0; st < 3; ++st) {
             mbar_init(&ctl->raw[st], 1);
             mbar_init(&ctl->conv[st], 1);
             mbar_init(&ctl->free_[st], KDP_WARPS);

@@ -139,8 +139,9 @@ static bool make_tiling(const hgm_scene *sc, const hgm_offsets &o, int T, int NM
     const char *benv = getenv("HGM_SMEM_KB");  // tuning knob: shared memory per CTA (2 CTAs per SM by default)
     // (shared-memory budget, stages): 2 CTAs/SM double-buffered; 1 CTA/SM double-buffered;
     // 1 CTA/SM single stage (items too large for two, i.e. large T)
+    const char *nenv = getenv("HGM_STAGES");  // tuning knob: stages of the first budget (2 or 3)
     const size_t budgets[3] = {(size_t)(benv ? atoi(benv) : 110) * 1024, 220 * 1024, 220 * 1024};
-    const int stages[3] = {2, 2, 1};
+    const int stages[3] = {nenv ? std::max(1, std::min(3, atoi(nenv))) : 2, 2, 1};
     // stage bytes of the unclipped item: b-frames [a, b), a-frames [g0, g1)
     auto foot = [&](int64_t a, int64_t b, int64_t g0, int64_t g1, int64_t book) {
         return (int64_t)item_stage_bytes((int)(QP(b) - QP(a)), (int)(QP(g1) - QP(g0)), (int)(NF(b + T - 1) - NF(a)),
