@@ -56,7 +56,7 @@ struct Seg {  // one (b-frame f, a-frame f-g) block of real states
     unsigned inv;  // ceil(2^32 / nb): division-free state decode
 };
 
-constexpr int KDP_THREADS = 256;               // compute warps
+constexpr int KDP_THREADS = 256;               // compute warps (12 measured 3 % slower)
 constexpr int KDP_WARPS = KDP_THREADS / 32;
 constexpr int KDP_BLOCK = KDP_THREADS + 32;      // + one copy warp (claims items, issues their TMA copies)
 constexpr int NROWI = 6;  // derived row bookkeeping ints per row

@@ -140,7 +140,9 @@ static bool make_tiling(const hgm_scene *sc, const hgm_offsets &o, int T, int NM
     // (shared-memory budget, stages): 2 CTAs/SM double-buffered; 1 CTA/SM double-buffered;
     // 1 CTA/SM single stage (items too large for two, i.e. large T)
     const char *nenv = getenv("HGM_STAGES");  // tuning knob: stages of the first budget (2 or 3)
-    const size_t budgets[3] = {(size_t)(benv ? atoi(benv) : 110) * 1024, 220 * 1024, 220 * 1024};
+    size_t budgets[3] = {(size_t)(benv ? atoi(benv) : 110) * 1024, 220 * 1024, 220 * 1024};
+    if (const char *menv = getenv("HGM_SMEM_MAX_KB"))  // testing: cap every budget (forces the fallbacks)
+        for (size_t &b : budgets) b = std::min(b, (size_t)atoi(menv) * 1024);
     const int stages[3] = {nenv ? std::max(1, std::min(3, atoi(nenv))) : 2, 2, 1};
     // stage bytes of the unclipped item: b-frames [a, b), a-frames [g0, g1)
     auto foot = [&](int64_t a, int64_t b, int64_t g0, int64_t g1, int64_t book) {

@@ -245,6 +245,27 @@ def test_model_batched_kernel_bitexact(hgm, name, kw, monkeypatch):
         assert torch.equal(a.E_all, b.E_all) and torch.equal(a.winner, b.winner) and torch.equal(a.score, b.score)
 
 
+def test_dense_fallbacks_bitexact(hgm, monkeypatch):
+    """Shared memory capped so that no tiling fits: detect_actions retries its 6-model
+    batch one model at a time and each model falls back to the reference (v0) kernels;
+    with a cap that only fits one model, the single-model tiled path runs.  Both must
+    give the bits of the v0 kernels."""
+    import torch
+
+    wl = synth.make_workload("C2")
+    p = wl.params()
+    s = hgm.build_scene_index(wl.scenes[1], device=0, T_max=10)
+    models = [hgm.build_model_graph(m, device=0) for m in wl.models]
+    monkeypatch.setenv("HGM_KERNEL", "v0")
+    ref = hgm.detect_actions(models, s, p, 0, 1, 80, wl.window, want_E_all=True)
+    monkeypatch.setenv("HGM_KERNEL", "v1")
+    for cap in ("4", "40", "64"):
+        monkeypatch.setenv("HGM_SMEM_MAX_KB", cap)
+        got = hgm.detect_actions(models, s, p, 0, 1, 80, wl.window, want_E_all=True)
+        torch.cuda.synchronize()
+        assert torch.equal(ref.E_all, got.E_all) and torch.equal(ref.winner, got.winner), cap
+
+
 @pytest.mark.parametrize("smem_kb", [20, 32, 48, 110])
 def test_tile_sizes_bitexact(hgm, smem_kb, monkeypatch):
     """Shared-memory budgets from tiny (one-frame tiles whose a-frames are split into
