@@ -115,6 +115,25 @@ hgm_status hgm_detect_actions(const hgm_model *const *models, int32_t n_models, 
                               const hgm_params *params, const hgm_offsets *offsets, int32_t score_mode,
                               float threshold, int32_t *winner, float *score, float *E_all, void *stream);
 
+/* Recognition ("nearest prototype classifier (NPC)" with the
+ * appearance distance only, P:L739-743 blocks of 60 frames; SPEC classify / split_blocks):
+ * every prototype is matched against every block (block k = frames
+ * [first_frame + k*stride, ... + window), the `offsets` of detect) and scored by its
+ * appearance distance A (R14).
+ *   block_label[k] = label[m*] of the nearest prototype m* (ties -> lowest prototype
+ *                    index), -1 if its distance exceeds `threshold` (+inf: none);
+ *   block_score[k] = that distance;
+ *   *clip_label    = majority vote over the labelled blocks (ties -> smallest label),
+ *                    -1 if no block is labelled.
+ * label: host array [n_prototypes] of values in [0, n_labels), n_labels <= 4096.
+ * block_label / block_score / clip_label: host or device pointers (NULL: not written).
+ * Errors: as hgm_detect_actions; a label outside [0, n_labels) or n_labels out of range
+ * -> INVALID_ARGUMENT. */
+hgm_status hgm_classify_blocks(const hgm_model *const *prototypes, int32_t n_prototypes, const int32_t *label,
+                               int32_t n_labels, const hgm_scene *scene, const hgm_params *params,
+                               const hgm_offsets *blocks, float threshold, int32_t *block_label,
+                               float *block_score, int32_t *clip_label, void *stream);
+
 /* Kernel timing (CUDA events on the launch stream) for the roofline report.
  * When enabled, every call accumulates per-kernel-class device time.
  * Classes: 0 scene index (incl. K-G), 1 model graph, 2 unary table (K-U),

@@ -281,3 +281,43 @@ def detect(models_pts, scene_pts, params: dict, first_frame: int, stride: int, c
             winner[k] = w if col[w] <= threshold else -1
             score[k] = col[w]
     return DetectResult(winner, score, EE, ER, AA, ZZ)
+
+
+# ----------------------------------------------------------------- recognition
+@dataclass
+class ClassifyResult:
+    block_label: np.ndarray  # int32 [n_blocks], -1 = no prototype within threshold
+    block_score: np.ndarray  # float64 [n_blocks]: appearance distance of the nearest prototype
+    block_proto: np.ndarray  # int32 [n_blocks]: index of the nearest prototype (-1 as above)
+    clip_label: int  # majority vote over labelled blocks, ties -> smallest label; -1 if none
+    A: np.ndarray  # float64 [n_prototypes, n_blocks]
+
+
+def majority_vote(labels) -> int:
+    """SPEC 'per-block classification aggregates to a stream label by majority
+    vote over blocks' (DESIGN.md reading R-f1b: ties -> smallest label;
+    unlabelled blocks (-1) abstain; no labelled block -> -1)."""
+    counts = {}
+    for l in labels:
+        l = int(l)
+        if l >= 0:
+            counts[l] = counts.get(l, 0) + 1
+    if not counts:
+        return -1
+    top = max(counts.values())
+    return min(l for l, c in counts.items() if c == top)
+
+
+def classify_blocks(prototypes_pts, labels, scene_pts, params: dict, first_frame: int, stride: int, count: int,
+                    window: int, threshold: float = float("inf"), n_threads=None) -> ClassifyResult:
+    """Nearest prototype classifier (Sec. 4): every prototype is
+    matched against every scene block (block k = frames [first_frame + k*stride,
+    + window), L739-743 '60 frames'), the distance is the appearance part A of the
+    optimal assignment ('only the appearance terms U(.) are used', L712), the block
+    takes the label of the nearest prototype (lowest index on ties, D-12) and the
+    clip label is the majority vote over blocks (SPEC)."""
+    r = detect(prototypes_pts, scene_pts, params, first_frame, stride, count, window, score_mode=1,
+               threshold=threshold, n_threads=n_threads)
+    labels = np.asarray(labels, dtype=np.int32)
+    bl = np.where(r.winner >= 0, labels[np.maximum(r.winner, 0)], -1).astype(np.int32)
+    return ClassifyResult(bl, r.score, r.winner, majority_vote(bl), r.A)

@@ -449,6 +449,42 @@ hgm_status hgm_detect_actions(const hgm_model *const *models, int32_t n_models, 
     return HGM_OK;
 }
 
+hgm_status hgm_classify_blocks(const hgm_model *const *prototypes, int32_t n_prototypes, const int32_t *label,
+                               int32_t n_labels, const hgm_scene *scene, const hgm_params *params,
+                               const hgm_offsets *blocks, float threshold, int32_t *block_label, float *block_score,
+                               int32_t *clip_label, void *stream) {
+    if (!prototypes || !scene || !params || !blocks) return fail(HGM_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (n_prototypes < 1) return fail(HGM_ERR_EMPTY_POINT_SET, "empty prototype dictionary");
+    if (!label) return fail(HGM_ERR_INVALID_ARGUMENT, "label == NULL");
+    if (n_labels < 1 || n_labels > 4096) return fail(HGM_ERR_INVALID_ARGUMENT, "n_labels must be 1..4096");
+    for (int m = 0; m < n_prototypes; ++m)
+        if (label[m] < 0 || label[m] >= n_labels) return fail(HGM_ERR_INVALID_ARGUMENT, "label out of range");
+    HGM_TRY(check_offsets(blocks));
+    const int count = blocks->count;
+    cudaStream_t s = (cudaStream_t)stream;
+    HGM_CUDA(cudaSetDevice(scene->device));
+    DevBuf win, sco, lab, bl, cl;
+    HGM_TRY(win.alloc(sizeof(int32_t) * std::max(count, 1), s));
+    const bool hs = block_score && !is_device_ptr(block_score);
+    if (hs || !block_score) HGM_TRY(sco.alloc(sizeof(float) * std::max(count, 1), s));
+    float *sd = (hs || !block_score) ? sco.as<float>() : block_score;
+    HGM_TRY(hgm_detect_actions(prototypes, n_prototypes, scene, params, blocks, /*score_mode=*/1, threshold,
+                               win.as<int32_t>(), sd, nullptr, stream));
+    HGM_TRY(lab.alloc(sizeof(int32_t) * n_prototypes, s));
+    HGM_CUDA(cudaMemcpyAsync(lab.p, label, sizeof(int32_t) * n_prototypes, cudaMemcpyHostToDevice, s));
+    const bool hb = block_label && !is_device_ptr(block_label), hc = clip_label && !is_device_ptr(clip_label);
+    if (hb) HGM_TRY(bl.alloc(sizeof(int32_t) * std::max(count, 1), s));
+    if (hc) HGM_TRY(cl.alloc(sizeof(int32_t), s));
+    HGM_TRY(block_vote(win.as<int32_t>(), count, lab.as<int32_t>(), n_labels, hb ? bl.as<int32_t>() : block_label,
+                       hc ? cl.as<int32_t>() : clip_label, s));
+    HGM_CUDA(cudaGetLastError());
+    if (hb) HGM_CUDA(cudaMemcpyAsync(block_label, bl.p, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, s));
+    if (hc) HGM_CUDA(cudaMemcpyAsync(clip_label, cl.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    if (hs) HGM_CUDA(cudaMemcpyAsync(block_score, sco.p, sizeof(float) * count, cudaMemcpyDeviceToHost, s));
+    HGM_CUDA(cudaStreamSynchronize(s));  // the label array (host) and the scratch are released here
+    return HGM_OK;
+}
+
 hgm_status hgm_set_profiling(int enable) {
     std::lock_guard<std::mutex> lk(g_mu);
     g_prof = enable != 0;

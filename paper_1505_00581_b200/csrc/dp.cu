@@ -225,6 +225,41 @@ __global__ void k_offset_argmin(const float *__restrict__ score, int nm, int cou
     if (best) best[k] = v;
 }
 
+// Recognition vote (f1): block label = label of the block's winning prototype (-1 if
+// none); clip label = majority over labelled blocks, ties -> smallest label.  One CTA.
+__global__ void __launch_bounds__(256) k_block_vote(const int32_t *__restrict__ winner, int count,
+                                                    const int32_t *__restrict__ label, int n_labels,
+                                                    int32_t *block_label, int32_t *clip_label) {
+    extern __shared__ unsigned hist_[];  // [n_labels]
+    for (int q = threadIdx.x; q < n_labels; q += blockDim.x) hist_[q] = 0;
+    __syncthreads();
+    for (int k = threadIdx.x; k < count; k += blockDim.x) {
+        const int w = winner[k];
+        const int l = w >= 0 ? label[w] : -1;
+        if (block_label) block_label[k] = l;
+        if (l >= 0) atomicAdd(&hist_[l], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // argmax, ties to the smallest label: key = count << 32 | ~label
+        unsigned long long best = 0;
+        for (int q = threadIdx.x; q < n_labels; q += 32) {
+            const unsigned long long key = ((unsigned long long)hist_[q] << 32) | (0xffffffffu - (unsigned)q);
+            if (hist_[q] > 0 && key > best) best = key;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long y = __shfl_xor_sync(0xffffffffu, best, o);
+            if (y > best) best = y;
+        }
+        if (threadIdx.x == 0 && clip_label) *clip_label = best ? (int)(0xffffffffu - (unsigned)(best & 0xffffffffu)) : -1;
+    }
+}
+
+hgm_status block_vote(const int32_t *winner, int count, const int32_t *label, int n_labels, int32_t *block_label,
+                      int32_t *clip_label, cudaStream_t s) {
+    k_block_vote<<<1, 256, sizeof(unsigned) * n_labels, s>>>(winner, count, label, n_labels, block_label, clip_label);
+    return HGM_OK;
+}
+
 hgm_status offset_argmin(const float *score, int n_models, int count, float threshold, int32_t *winner, float *best,
                          cudaStream_t s) {
     if (count <= 0) return HGM_OK;

@@ -22,7 +22,7 @@ STATUS = {0: "HGM_OK", 1: "HGM_ERR_EMPTY_POINT_SET", 2: "HGM_ERR_DIMENSION_MISMA
 
 EXPORTS = ("hgm_build_model_graph", "hgm_build_model_graph_dev", "hgm_model_num_nodes", "hgm_free_model",
            "hgm_build_scene_index", "hgm_build_scene_index_dev", "hgm_scene_num_nodes", "hgm_free_scene",
-           "hgm_match_model_at_offsets", "hgm_detect_actions", "hgm_set_profiling", "hgm_get_stats",
+           "hgm_match_model_at_offsets", "hgm_detect_actions", "hgm_classify_blocks", "hgm_set_profiling", "hgm_get_stats",
            "hgm_last_error", "hgm_version")
 
 
@@ -80,6 +80,8 @@ def lib():
         L.hgm_match_model_at_offsets.argtypes = [vp, vp, P(Params), P(Offsets), vp, vp, vp, vp]
         L.hgm_detect_actions.argtypes = [P(vp), C.c_int32, vp, P(Params), P(Offsets), C.c_int32, C.c_float, vp, vp,
                                          vp, vp]
+        L.hgm_classify_blocks.argtypes = [P(vp), C.c_int32, vp, C.c_int32, vp, P(Params), P(Offsets), C.c_float,
+                                          vp, vp, vp, vp]
         L.hgm_set_profiling.argtypes = [C.c_int]
         L.hgm_get_stats.argtypes = [P(Stats), C.c_int]
         L.hgm_last_error.restype = C.c_char_p
@@ -284,6 +286,33 @@ def detect_actions(models, scene: Scene, params=None, first_frame=0, stride=1, c
     _check(lib().hgm_detect_actions(handles, nm, scene.h, C.byref(_params(params)), C.byref(o), int(score_mode),
                                     float(threshold), _ptr(winner), _ptr(score), _ptr(E_all), _stream_ptr(stream)))
     return DetectResult(winner, score, E_all)
+
+
+@dataclass
+class ClassifyResult:
+    block_label: object  # int32 [count]
+    block_score: object  # float32 [count]: appearance distance of the nearest prototype
+    clip_label: int  # majority vote, -1 if no block is labelled
+
+
+def classify_blocks(prototypes, labels, scene: Scene, params=None, first_frame=0, stride=60, count=1, window=60,
+                    threshold=math.inf, n_labels=None, stream=None) -> ClassifyResult:
+    """Nearest-prototype recognition per scene block + majority vote
+    (hgm_classify_blocks).  Host outputs."""
+    nm = len(prototypes)
+    lab = np.ascontiguousarray(labels, dtype=np.int32)
+    if lab.shape != (nm,):
+        raise ValueError("labels must have one entry per prototype")
+    n_labels = int(lab.max()) + 1 if n_labels is None else int(n_labels)
+    bl = np.empty(count, np.int32)
+    bs = np.empty(count, np.float32)
+    cl = np.empty(1, np.int32)
+    handles = (C.c_void_p * nm)(*[m.h.value for m in prototypes])
+    o = Offsets(int(first_frame), int(stride), int(count), int(window))
+    _check(lib().hgm_classify_blocks(handles, nm, lab.ctypes.data, n_labels, scene.h, C.byref(_params(params)),
+                                     C.byref(o), float(threshold), _ptr(bl), _ptr(bs), _ptr(cl),
+                                     _stream_ptr(stream)))
+    return ClassifyResult(bl, bs, int(cl[0]))
 
 
 def set_profiling(enable: bool = True):

@@ -18,6 +18,8 @@ from .kth import (  # noqa: F401
     F_KTH,
     gen_model,
     gen_clutter,
+    make_recognition,
+    RecognitionSet,
     gen_planted,
     concat_points,
     make_workload,

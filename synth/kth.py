@@ -281,3 +281,57 @@ def make_workload(name: str, seed: int = 0, T: int | None = None, frame_range=No
                                      frame_range)
         return Workload(name, models, [scene], 400, 10, 0, [(nf - 400) // 10 + 1], T=T, first=[0])
     raise ValueError(f"unknown config {name}")
+
+
+@dataclass
+class RecognitionSet:
+    """A prototype dictionary and one scene clip cut into blocks."""
+
+    prototypes: list[Points]
+    labels: np.ndarray  # int32 [n_prototypes]
+    scene: Points
+    block: int  # block length in frames (= window)
+    stride: int
+    count: int  # number of blocks
+    truth: np.ndarray  # int32 [count]: class planted in block k
+    T: int = 10
+
+    def params(self) -> dict:
+        return dict(lambda1=0.6, lambda2=0.2, lambda3=5.0, w_dummy=1.0, T=self.T)
+
+
+def make_recognition(seed: int = 0, n_classes: int = N_CLASSES, protos_per_class: int = 2, count: int = 8,
+                     block: int = 60, model_frames: int = 30, pts_per_frame: int = 2, F: int = F_KTH,
+                     rho: float = 5.0, T: int = 10, exact: bool = False, clip_class: int | None = None,
+                     class_of_block=None) -> RecognitionSet:
+    """Prototypes: `protos_per_class` sub-sequence models per class (PAPER.md L712:
+    'augmented the number of model graph prototypes'), labels = class.  Scene:
+    `count` consecutive blocks of `block` frames (L739: 60-frame blocks), Poisson
+    clutter plus one planted instance of prototype (class c, stream 0) per block,
+    c = clip_class, or class_of_block(k), or drawn.  exact=True plants unwarped,
+    noise-free, jitter-free copies (distance 0 to their prototype)."""
+    cfg = f"R:{seed}"
+    protos, labels = [], []
+    for c in range(n_classes):
+        for s in range(protos_per_class):
+            protos.append(gen_model(c, model_frames, pts_per_frame, F, cfg, s,
+                                    gap2_prob=0.0 if exact else 0.15))
+            labels.append(c)
+    rng = _rng(cfg, 9)
+    parts, truth = [], []
+    for k in range(count):
+        c = clip_class if clip_class is not None else (
+            class_of_block(k) if class_of_block is not None else int(rng.integers(0, n_classes)))
+        truth.append(c)
+        f0 = k * block
+        parts.append(gen_clutter(block, f0, rho, F, rng))
+        m = protos[c * protos_per_class]
+        room = block - (_span(m) + _span(m) // 2 + 2) if not exact else block - _span(m)
+        start = f0 + int(rng.integers(0, max(room, 0) + 1))
+        if exact:
+            parts.append(Points((m.frame - m.frame.min() + start).astype(np.int32), m.x.copy(), m.y.copy(),
+                                m.saliency.copy(), m.feat.copy()))
+        else:
+            parts.append(gen_planted(m, start, T, rng))
+    return RecognitionSet(protos, np.array(labels, np.int32), concat_points(parts), block, block, count,
+                          np.array(truth, np.int32), T)

@@ -296,3 +296,46 @@ def test_bit_determinism(hgm):
     b = hgm.match_model_at_offsets(m, s, p, 0, 1, 541, 60)
     torch.cuda.synchronize()
     assert torch.equal(a.E, b.E) and torch.equal(a.A, b.A) and torch.equal(a.z, b.z)
+
+
+@pytest.mark.parametrize("seed,exact", [(0, False), (1, False), (2, True)])
+def test_classify_blocks_matches_oracle(hgm, seed, exact):
+    """Recognition layer (f1): per-block labels / distances and the clip vote against
+    oracle.classify_blocks; 6 classes x 2 prototypes (M=30), 8 blocks of 60 frames."""
+    rs = synth.make_recognition(seed, count=8, exact=exact)
+    p = rs.params()
+    ref = oracle.classify_blocks(rs.prototypes, rs.labels, rs.scene, p, 0, rs.stride, rs.count, rs.block)
+    scene = hgm.build_scene_index(rs.scene, device=0, T_max=p["T"])
+    protos = [hgm.build_model_graph(m, device=0) for m in rs.prototypes]
+    got = hgm.classify_blocks(protos, rs.labels, scene, p, 0, rs.stride, rs.count, rs.block)
+    for k in range(rs.count):
+        assert abs(float(got.block_score[k]) - ref.block_score[k]) <= tol(ref.block_score[k]), k
+        if got.block_label[k] != ref.block_label[k]:  # only a near-tie between the two nearest may differ
+            a = ref.A[:, k]
+            w = int(np.argmin(np.where(rs.labels == got.block_label[k], a, np.inf)))
+            assert abs(a[w] - a[ref.block_proto[k]]) <= tol(a[ref.block_proto[k]]), k
+    assert got.clip_label == oracle.majority_vote(got.block_label)
+    if exact:
+        assert np.array_equal(got.block_label, rs.truth) and np.all(got.block_score == 0)
+    # the distances equal the appearance scores of detect_actions(score_mode=1)
+    det = hgm.detect_actions(protos, scene, p, 0, rs.stride, rs.count, rs.block, score_mode=1, device_out=False)
+    assert np.array_equal(det.score, got.block_score)
+    assert np.array_equal(np.where(det.winner >= 0, rs.labels[np.maximum(det.winner, 0)], -1), got.block_label)
+
+
+def test_classify_blocks_threshold_and_errors(hgm):
+    rs = synth.make_recognition(5, count=6)
+    p = rs.params()
+    scene = hgm.build_scene_index(rs.scene, device=0, T_max=p["T"])
+    protos = [hgm.build_model_graph(m, device=0) for m in rs.prototypes]
+    full = hgm.classify_blocks(protos, rs.labels, scene, p, 0, rs.stride, rs.count, rs.block)
+    thr = float(np.median(full.block_score))
+    r = hgm.classify_blocks(protos, rs.labels, scene, p, 0, rs.stride, rs.count, rs.block, threshold=thr)
+    assert np.array_equal(r.block_label, np.where(full.block_score <= thr, full.block_label, -1))
+    assert r.clip_label == oracle.majority_vote(r.block_label)
+    r = hgm.classify_blocks(protos, rs.labels, scene, p, 0, rs.stride, rs.count, rs.block, threshold=-1.0)
+    assert np.all(r.block_label == -1) and r.clip_label == -1
+    bad = rs.labels.copy()
+    bad[0] = 6
+    with pytest.raises(hgm.HGMError):
+        hgm.classify_blocks(protos, bad, scene, p, 0, rs.stride, rs.count, rs.block, n_labels=6)
