@@ -717,7 +717,11 @@ __global__ void __launch_bounds__(256) k_item_prep(SceneView sc, const WorkItem 
     uint8_t *smap = bk + bp.map;
     __shared__ int s_cnt[256];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int F0 = w.F0, F1 = w.F1, nseg = (F1 - F0) * (T - 1);
+    // segments (b-frame f, gap g) whose a-frame f - g lies in the item's chunk [G0, G1):
+    // gaps [gmin, gmax]; the host keeps (F1 - F0) * (gmax - gmin + 1) <= 255 (uint8 map)
+    const int F0 = w.F0, F1 = w.F1;
+    const int gmin = max(1, F0 - w.G1 + 1), gmax = min(T - 1, F1 - 1 - w.G0);
+    const int nseg = max(0, (F1 - F0) * (gmax - gmin + 1));
     const int th0 = w.qa & ~3;  // theta_pad index the stage's TH[0] holds (the copy starts 16-byte aligned)
     for (int r = tid; r < w.B1 - w.A0; r += blockDim.x) {
         const int x = w.A0 + r;
@@ -732,7 +736,7 @@ __global__ void __launch_bounds__(256) k_item_prep(SceneView sc, const WorkItem 
     Seg sg{};
     int cnt = 0;
     if (tid < nseg) {  // segments, gap-major: long candidate ranges first
-        const int g = 1 + tid / (F1 - F0);
+        const int g = gmin + tid / (F1 - F0);
         const int f = F0 + tid % (F1 - F0);
         if (f - g >= w.d.o && f - g >= w.G0 && f - g < w.G1) {
             sg.g = g;

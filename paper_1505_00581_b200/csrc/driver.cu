@@ -180,13 +180,15 @@ static bool make_tiling(const hgm_scene *sc, const hgm_offsets &o, int T, int NM
                 while (F1 < f_hi && F1 - F0 < FT_max && foot(F0, F1 + 1, F0 - T + 1, F1 + 1, book) <= cap) ++F1;
                 t.gstart.push_back((int32_t)F0);
                 t.sub_begin.push_back((int32_t)(t.sub_g.size() / 2));
-                if (foot(F0, F1, F0 - T + 1, F1, book) <= cap) {
+                if ((F1 - F0) * (T - 1) <= 255 && foot(F0, F1, F0 - T + 1, F1, book) <= cap) {
                     account(F0, F1, F0 - T + 1, F1);  // one item covers every a-frame
                 } else {  // large T (only a single b-frame gets here): its a-frames [F0 - T + 1, F1) in chunks
                     for (int64_t G0 = F0 - T + 1; G0 < F1 && fits;) {
                         int64_t G1 = G0 + 1;
                         if (foot(F0, F1, G0, G1, book) > cap) fits = false;
-                        while (G1 < F1 && foot(F0, F1, G0, G1 + 1, book) <= cap) ++G1;
+                        // <= 255 segments per item (k_item_prep's uint8 state -> segment map)
+                        while (G1 < F1 && (G1 + 1 - G0) * (F1 - F0) <= 255 && foot(F0, F1, G0, G1 + 1, book) <= cap)
+                            ++G1;
                         account(F0, F1, G0, G1);
                         G0 = G1;
                     }

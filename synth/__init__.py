@@ -19,6 +19,7 @@ from .kth import (  # noqa: F401
     gen_model,
     gen_clutter,
     make_recognition,
+    make_single,
     RecognitionSet,
     gen_planted,
     concat_points,

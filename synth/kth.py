@@ -335,3 +335,26 @@ def make_recognition(seed: int = 0, n_classes: int = N_CLASSES, protos_per_class
             parts.append(gen_planted(m, start, T, rng))
     return RecognitionSet(protos, np.array(labels, np.int32), concat_points(parts), block, block, count,
                           np.array(truth, np.int32), T)
+
+
+def make_single(seed: int = 0, n_frames: int = 723, n_nodes: int = 754, model_frames: int = 30, F: int = F_KTH,
+                T: int = 10, plant: bool = True) -> Workload:
+    """The paper's single-instance regime (Table 3): ONE model of
+    30 nodes (1 point per frame) against a whole scene video of `n_nodes` nodes over
+    `n_frames` frames (754 / 723), one window covering the whole video.  Scene: one
+    clutter point in every frame, the remaining n_nodes - n_frames points in random
+    frames, and one planted warped copy of the model; the planted points replace
+    clutter so the node count stays n_nodes (up to the model's size)."""
+    cfg = f"S:{seed}"
+    model = gen_model(0, model_frames, 1, F, cfg, 0)
+    rng = _rng(cfg, 4)
+    span = _span(model)
+    start = int(rng.integers(0, max(n_frames - 2 * span, 0) + 1))
+    planted = gen_planted(model, start, T, rng) if plant else gen_clutter(0, 0, 0.0, F, rng, exact_count=0)
+    n_extra = max(n_nodes - n_frames - planted.n, 0)
+    fr = np.sort(np.concatenate([np.arange(n_frames), rng.integers(0, n_frames, size=n_extra)]))
+    clutter = gen_clutter(n_frames, 0, 0.0, F, rng, exact_count=fr.shape[0])
+    clutter.frame[:] = fr
+    scene = concat_points([clutter, planted])
+    return Workload("single", [model], [scene], window=n_frames, stride=1, first_frame=0, count=[1], T=T,
+                    first=[0])

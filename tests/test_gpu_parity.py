@@ -339,3 +339,50 @@ def test_classify_blocks_threshold_and_errors(hgm):
     bad[0] = 6
     with pytest.raises(hgm.HGMError):
         hgm.classify_blocks(protos, bad, scene, p, 0, rs.stride, rs.count, rs.block, n_labels=6)
+
+
+def _single_check(hgm, wl, T, oracle_ref=True):
+    p = wl.params()
+    p["T"] = T
+    chk = Checker(wl.models, wl.scenes[0], p, 0, 1, wl.window)
+    scene = hgm.build_scene_index(wl.scenes[0], device=0, T_max=T)
+    m = hgm.build_model_graph(wl.models[0], device=0)
+    r = hgm.match_model_at_offsets(m, scene, p, 0, 1, 1, wl.window, device_out=False)
+    if oracle_ref:
+        E_o, _, A_o, z_o = chk.oracle_pairs([(0, 0)])
+        msg = chk.check_pair(0, 0, r.E[0], r.A[0], r.z[0], E_o[0], A_o[0], z_o[0])
+        assert msg in (None, "TIE"), msg
+    return r, chk
+
+
+@pytest.mark.parametrize("T,plant", [(10, True), (10, False), (40, False), (80, True)])
+def test_single_instance_754_nodes(hgm, T, plant):
+    """f2: one M=30 model against a whole 754-node / 723-frame scene in one window
+    (Table 3), against the oracle."""
+    _single_check(hgm, synth.make_single(0 if plant else 1, plant=plant), T)
+
+
+@pytest.mark.parametrize("seed,plant", [(0, True), (2, False)])
+def test_single_instance_unpruned(hgm, seed, plant):
+    """f2, T = +inf: a 160-frame scene with T above its span,
+    against the oracle (its O(S^3 M) cost bounds the size)."""
+    wl = synth.make_single(seed, n_frames=160, n_nodes=190, plant=plant)
+    _single_check(hgm, wl, 161)
+
+
+def test_single_instance_unpruned_full_size_properties(hgm):
+    """T = +inf at the paper's full size (754 nodes): the GPU assignment is feasible, its
+    fp64 energy (oracle.energy) equals the GPU E*, and E*(inf) <= E*(80) <= E*(10)."""
+    wl = synth.make_single(1, plant=False)
+    Es = []
+    for T in (10, 80, 724):
+        r, chk = _single_check(hgm, wl, T, oracle_ref=False)
+        Es.append(float(r.E[0]))
+        wb, we = chk.window_of(0)
+        win = chk.scene.slice(wb, we)
+        zl = np.array([-1 if v < 0 else chk.id2pos[int(v)] - wb for v in r.z[0]], np.int32)
+        p = dict(chk.params)
+        assert oracle.feasible(chk.models[0], win, p, zl)
+        Ez = oracle.energy(chk.models[0], win, p, zl)
+        assert abs(Ez - Es[-1]) <= tol(Ez), (T, Ez, Es[-1])
+    assert Es[2] <= Es[1] + tol(Es[1]) and Es[1] <= Es[0] + tol(Es[0]), Es
