@@ -77,6 +77,15 @@ typedef struct {
  * Errors: n == 0 -> EMPTY_POINT_SET; NULL arrays / F < 1 -> INVALID_ARGUMENT. */
 hgm_status hgm_build_model_graph(const hgm_points *pts, int device, hgm_model **out);
 hgm_status hgm_build_model_graph_dev(const hgm_points *pts, void *stream, hgm_model **out);
+/* Independent chains ("Multiple points 2: creation of
+ * several single point models (several second order chains), each of which is solved
+ * independently"): chain `rank` keeps, per frame, the point of saliency rank `rank`
+ * (0 = most salient, i.e. hgm_build_model_graph; ties: earlier input point first);
+ * frames with <= rank points have no node.  Same host-memory input as
+ * hgm_build_model_graph; synchronous.
+ * Errors: as hgm_build_model_graph; rank < 0 -> INVALID_ARGUMENT; no frame with more
+ * than `rank` points -> EMPTY_POINT_SET. */
+hgm_status hgm_build_model_chain(const hgm_points *pts, int device, int32_t rank, hgm_model **out);
 hgm_status hgm_model_num_nodes(const hgm_model *model, int32_t *M);
 void hgm_free_model(hgm_model *model);
 
@@ -114,6 +123,19 @@ hgm_status hgm_match_model_at_offsets(const hgm_model *model, const hgm_scene *s
 hgm_status hgm_detect_actions(const hgm_model *const *models, int32_t n_models, const hgm_scene *scene,
                               const hgm_params *params, const hgm_offsets *offsets, int32_t score_mode,
                               float threshold, int32_t *winner, float *score, float *E_all, void *stream);
+
+/* Detection with multi-chain models (f3): `chains` [n_chains] are the
+ * chains of n_models models, grouped (chain_model: host [n_chains], non-decreasing,
+ * every model in [0, n_models) present).  The distance of model m at offset k is the
+ * mean over its chains of their score (E* for score_mode 0, A for 1, as
+ * hgm_detect_actions); winner / score as hgm_detect_actions over these means (ties ->
+ * lowest model); S_all (optional, [n_models][count]) receives the means.  Outputs host
+ * or device.  Errors: as hgm_detect_actions; chain_model NULL / out of range / not
+ * grouped -> INVALID_ARGUMENT; a model without a chain -> EMPTY_POINT_SET. */
+hgm_status hgm_detect_chains(const hgm_model *const *chains, int32_t n_chains, const int32_t *chain_model,
+                             int32_t n_models, const hgm_scene *scene, const hgm_params *params,
+                             const hgm_offsets *offsets, int32_t score_mode, float threshold, int32_t *winner,
+                             float *score, float *S_all, void *stream);
 
 /* Recognition ("nearest prototype classifier (NPC)" with the
  * appearance distance only, P:L739-743 blocks of 60 frames; SPEC classify / split_blocks):

@@ -131,6 +131,31 @@ def model_chain(frame, saliency) -> np.ndarray:
     return np.array([best[f] for f in sorted(best)], dtype=np.int64)
 
 
+def model_chain_rank(frame, saliency, rank: int) -> np.ndarray:
+    """Chain `rank` of the independent-chains model ("Multiple
+    points 2: creation of several single point models (several second order
+    chains)"): per occupied frame the point of saliency rank `rank` (0 = most
+    salient = model_chain; ties: earlier input point ranks first, D-1); frames with
+    <= rank points have no node.  Returns input indices ordered by frame."""
+    frame = np.asarray(frame)
+    saliency = np.asarray(saliency)
+    per = {}
+    for k in range(frame.shape[0]):  # plain scan in input order
+        per.setdefault(int(frame[k]), []).append(k)
+    out = []
+    for f in sorted(per):
+        ranked = sorted(per[f], key=lambda k: (-float(saliency[k]), k))
+        if rank < len(ranked):
+            out.append(ranked[rank])
+    return np.array(out, dtype=np.int64)
+
+
+def model_nodes_rank(pts, rank: int) -> NodeSet:
+    idx = model_chain_rank(pts.frame, pts.saliency, rank)
+    return NodeSet(pts.frame[idx].astype(np.int32), pts.x[idx].astype(np.float64),
+                   pts.y[idx].astype(np.float64), pts.feat[idx].astype(np.float64))
+
+
 def model_nodes(pts) -> NodeSet:
     idx = model_chain(pts.frame, pts.saliency)
     return NodeSet(pts.frame[idx].astype(np.int32), pts.x[idx].astype(np.float64),
@@ -321,3 +346,40 @@ def classify_blocks(prototypes_pts, labels, scene_pts, params: dict, first_frame
     labels = np.asarray(labels, dtype=np.int32)
     bl = np.where(r.winner >= 0, labels[np.maximum(r.winner, 0)], -1).astype(np.int32)
     return ClassifyResult(bl, r.score, r.winner, majority_vote(bl), r.A)
+
+
+# ------------------------------------------------------- independent chains
+def chain_points(pts, rank: int):
+    """The raw points of chain `rank` as a point set of the same type (so that
+    detect() can take it as a model): rank-r selection, then model_chain of it is
+    the identity (one point per frame)."""
+    return pts.take(model_chain_rank(pts.frame, pts.saliency, rank))
+
+
+def detect_chains(models_pts, n_chains: int, scene_pts, params: dict, first_frame: int, stride: int, count: int,
+                  window: int, score_mode: int = 0, threshold: float = float("inf"), n_threads=None):
+    """PAPER.md L756-761 "Multiple points 2": each model becomes up to n_chains single
+    point chains (chain_points, ranks no frame reaches dropped), every chain is matched
+    independently, and a model's distance is the average over its chains; then the
+    per-offset nearest model (D-12 ties).  Returns (winner, score, S [n_models, count],
+    chain_model)."""
+    chains, chain_model = [], []
+    for m, pts in enumerate(models_pts):
+        for r in range(n_chains):
+            idx = model_chain_rank(pts.frame, pts.saliency, r)
+            if idx.size == 0:
+                break
+            chains.append(pts.take(idx))
+            chain_model.append(m)
+    r = detect(chains, scene_pts, params, first_frame, stride, count, window, score_mode=score_mode,
+               n_threads=n_threads)
+    Sc = r.E if score_mode == 0 else r.A
+    cm = np.array(chain_model)
+    S = np.stack([Sc[cm == m].mean(axis=0) for m in range(len(models_pts))])
+    winner = np.full(count, -1, dtype=np.int32)
+    score = np.full(count, np.nan)
+    for k in range(count):
+        w = int(np.argmin(S[:, k]))
+        winner[k] = w if S[w, k] <= threshold else -1
+        score[k] = S[w, k]
+    return winner, score, S, cm

@@ -269,7 +269,7 @@ hgm_status hgm_build_model_graph(const hgm_points *pts, int device, hgm_model **
     {
         DevPoints dp;
         HGM_TRY(dp.load(pts, sg.s));
-        st = model_build_device(&dp.v, sg.s, out);
+        st = model_build_device(&dp.v, 0, sg.s, out);
     }
     HGM_CUDA(cudaStreamSynchronize(sg.s));
     return st;
@@ -279,7 +279,25 @@ hgm_status hgm_build_model_graph_dev(const hgm_points *pts, void *stream, hgm_mo
     HGM_TRY(check_points(pts));
     if (!out) return fail(HGM_ERR_INVALID_ARGUMENT, "out == NULL");
     configure_pool();
-    return model_build_device(pts, (cudaStream_t)stream, out);
+    return model_build_device(pts, 0, (cudaStream_t)stream, out);
+}
+
+hgm_status hgm_build_model_chain(const hgm_points *pts, int device, int32_t rank, hgm_model **out) {
+    HGM_TRY(check_points(pts));
+    if (!out) return fail(HGM_ERR_INVALID_ARGUMENT, "out == NULL");
+    if (rank < 0) return fail(HGM_ERR_INVALID_ARGUMENT, "rank < 0");
+    HGM_CUDA(cudaSetDevice(device));
+    configure_pool();
+    StreamGuard sg;
+    sg.s = builder_stream(device);
+    hgm_status st;
+    {
+        DevPoints dp;
+        HGM_TRY(dp.load(pts, sg.s));
+        st = model_build_device(&dp.v, rank, sg.s, out);
+    }
+    HGM_CUDA(cudaStreamSynchronize(sg.s));
+    return st;
 }
 
 hgm_status hgm_model_num_nodes(const hgm_model *m, int32_t *M) {
@@ -375,37 +393,19 @@ hgm_status hgm_match_model_at_offsets(const hgm_model *model, const hgm_scene *s
     return HGM_OK;
 }
 
-hgm_status hgm_detect_actions(const hgm_model *const *models, int32_t n_models, const hgm_scene *scene,
-                              const hgm_params *params, const hgm_offsets *offsets, int32_t score_mode,
-                              float threshold, int32_t *winner, float *score, float *E_all, void *stream) {
-    if (!models || n_models <= 0) return fail(HGM_ERR_EMPTY_POINT_SET, "empty model dictionary");
-    if (!scene) return fail(HGM_ERR_INVALID_ARGUMENT, "NULL scene");
-    HGM_TRY(check_params(params, scene));
-    HGM_TRY(check_offsets(offsets));
-    if (score_mode != 0 && score_mode != 1) return fail(HGM_ERR_INVALID_ARGUMENT, "score_mode must be 0 or 1");
-    int M_total = 0;
-    for (int m = 0; m < n_models; ++m) {
-        if (!models[m]) return fail(HGM_ERR_INVALID_ARGUMENT, "NULL model handle");
-        if (models[m]->F != scene->F) return fail(HGM_ERR_DIMENSION_MISMATCH, "model and scene descriptor lengths differ");
-        M_total += models[m]->M;
-    }
+// E* and A of every (model, offset) into device matrices Ed / Ad [n_models][count].
+static hgm_status detect_scores(const hgm_model *const *models, int32_t n_models, const hgm_scene *scene,
+                                const hgm_params *params, const hgm_offsets *offsets, float *Ed, float *Ad,
+                                cudaStream_t s) {
     const int count = offsets->count;
-    if (count == 0) return HGM_OK;
-    cudaStream_t s = (cudaStream_t)stream;
-    HGM_CUDA(cudaSetDevice(scene->device));
     configure_pool();
     int64_t n_lo, n_hi;
     covered_range(scene, offsets, &n_lo, &n_hi);
     const int64_t nn = std::max<int64_t>(n_hi - n_lo, 1);
     const int Fp = scene->Fp;
-    DevBuf mfeat, U, Eb, Ab, zb, wdev, sdev;
+    DevBuf mfeat, U, zb;
     int Mmax = 0;
     for (int m = 0; m < n_models; ++m) Mmax = std::max(Mmax, models[m]->M);
-    (void)M_total;
-    const bool dEall = E_all && is_device_ptr(E_all);
-    HGM_TRY(Ab.alloc(sizeof(float) * (size_t)n_models * count, s));
-    if (!dEall) HGM_TRY(Eb.alloc(sizeof(float) * (size_t)n_models * count, s));
-    float *Ed = dEall ? E_all : Eb.as<float>();
     HGM_TRY(zb.alloc(sizeof(int64_t) * (size_t)count * Mmax * MAX_BATCH_API, s));
     // batches of consecutive models with equal chain length share one K-DP pass
     int max_batch = use_v0_kernels() ? 1 : MAX_BATCH_API;
@@ -421,7 +421,7 @@ hgm_status hgm_detect_actions(const hgm_model *const *models, int32_t n_models, 
         HGM_TRY(unary_table(mfeat.as<float>(), M, NM, Fp, scene, n_lo, n_hi, U.as<float>(), s));
         MatchOut mo[MAX_BATCH_API];
         for (int k = 0; k < NM; ++k)
-            mo[k] = MatchOut{Ed + (size_t)(m0 + k) * count, Ab.as<float>() + (size_t)(m0 + k) * count,
+            mo[k] = MatchOut{Ed + (size_t)(m0 + k) * count, Ad + (size_t)(m0 + k) * count,
                              zb.as<int64_t>() + (size_t)k * count * Mmax};
         g_tiling_failed = false;
         const hgm_status bst = match_batch(models + m0, NM, scene, *params, *offsets, U.as<float>(), n_lo, nn, mo, s);
@@ -435,17 +435,100 @@ hgm_status hgm_detect_actions(const hgm_model *const *models, int32_t n_models, 
     }
     scene->uses.record(s);
     for (int m = 0; m < n_models; ++m) models[m]->uses.record(s);
+    return HGM_OK;
+}
+
+static hgm_status check_dictionary(const hgm_model *const *models, int32_t n_models, const hgm_scene *scene,
+                                   const hgm_params *params, const hgm_offsets *offsets, int32_t score_mode) {
+    if (!models || n_models <= 0) return fail(HGM_ERR_EMPTY_POINT_SET, "empty model dictionary");
+    if (!scene) return fail(HGM_ERR_INVALID_ARGUMENT, "NULL scene");
+    HGM_TRY(check_params(params, scene));
+    HGM_TRY(check_offsets(offsets));
+    if (score_mode != 0 && score_mode != 1) return fail(HGM_ERR_INVALID_ARGUMENT, "score_mode must be 0 or 1");
+    for (int m = 0; m < n_models; ++m) {
+        if (!models[m]) return fail(HGM_ERR_INVALID_ARGUMENT, "NULL model handle");
+        if (models[m]->F != scene->F) return fail(HGM_ERR_DIMENSION_MISMATCH, "model and scene descriptor lengths differ");
+    }
+    return HGM_OK;
+}
+
+// per-offset argmin of S [n_models][count] into host-or-device outputs; S_all copied
+// out when the caller's pointer is a host one (a device S_all is already S).
+static hgm_status finish_detect(const float *S, int n_models, int count, float threshold, int32_t *winner,
+                                float *score, float *S_all, bool dSall, cudaStream_t s) {
+    DevBuf wdev, sdev;
     const bool hw = winner && !is_device_ptr(winner), hs = score && !is_device_ptr(score);
     if (hw) HGM_TRY(wdev.alloc(sizeof(int32_t) * count, s));
     if (hs) HGM_TRY(sdev.alloc(sizeof(float) * count, s));
-    HGM_TRY(offset_argmin(score_mode == 0 ? Ed : Ab.as<float>(), n_models, count, threshold,
-                          hw ? wdev.as<int32_t>() : winner, hs ? sdev.as<float>() : score, s));
+    HGM_TRY(offset_argmin(S, n_models, count, threshold, hw ? wdev.as<int32_t>() : winner,
+                          hs ? sdev.as<float>() : score, s));
     if (hw) HGM_CUDA(cudaMemcpyAsync(winner, wdev.p, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, s));
     if (hs) HGM_CUDA(cudaMemcpyAsync(score, sdev.p, sizeof(float) * count, cudaMemcpyDeviceToHost, s));
-    if (E_all && !dEall)
-        HGM_CUDA(cudaMemcpyAsync(E_all, Ed, sizeof(float) * (size_t)n_models * count, cudaMemcpyDeviceToHost, s));
-    if (hw || hs || (E_all && !dEall)) HGM_CUDA(cudaStreamSynchronize(s));
+    if (S_all && !dSall)
+        HGM_CUDA(cudaMemcpyAsync(S_all, S, sizeof(float) * (size_t)n_models * count, cudaMemcpyDeviceToHost, s));
+    if (hw || hs || (S_all && !dSall)) HGM_CUDA(cudaStreamSynchronize(s));
     HGM_CUDA(cudaGetLastError());
+    return HGM_OK;
+}
+
+hgm_status hgm_detect_actions(const hgm_model *const *models, int32_t n_models, const hgm_scene *scene,
+                              const hgm_params *params, const hgm_offsets *offsets, int32_t score_mode,
+                              float threshold, int32_t *winner, float *score, float *E_all, void *stream) {
+    HGM_TRY(check_dictionary(models, n_models, scene, params, offsets, score_mode));
+    const int count = offsets->count;
+    if (count == 0) return HGM_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    HGM_CUDA(cudaSetDevice(scene->device));
+    DevBuf Eb, Ab;
+    const bool dEall = E_all && is_device_ptr(E_all);
+    HGM_TRY(Ab.alloc(sizeof(float) * (size_t)n_models * count, s));
+    if (!dEall) HGM_TRY(Eb.alloc(sizeof(float) * (size_t)n_models * count, s));
+    float *Ed = dEall ? E_all : Eb.as<float>();
+    HGM_TRY(detect_scores(models, n_models, scene, params, offsets, Ed, Ab.as<float>(), s));
+    if (score_mode == 0) return finish_detect(Ed, n_models, count, threshold, winner, score, E_all, dEall, s);
+    HGM_TRY(finish_detect(Ab.as<float>(), n_models, count, threshold, winner, score, nullptr, false, s));
+    if (E_all && !dEall) {  // E_all always holds E*
+        HGM_CUDA(cudaMemcpyAsync(E_all, Ed, sizeof(float) * (size_t)n_models * count, cudaMemcpyDeviceToHost, s));
+        HGM_CUDA(cudaStreamSynchronize(s));
+    }
+    return HGM_OK;
+}
+
+hgm_status hgm_detect_chains(const hgm_model *const *chains, int32_t n_chains, const int32_t *chain_model,
+                             int32_t n_models, const hgm_scene *scene, const hgm_params *params,
+                             const hgm_offsets *offsets, int32_t score_mode, float threshold, int32_t *winner,
+                             float *score, float *S_all, void *stream) {
+    HGM_TRY(check_dictionary(chains, n_chains, scene, params, offsets, score_mode));
+    if (!chain_model) return fail(HGM_ERR_INVALID_ARGUMENT, "chain_model == NULL");
+    if (n_models < 1) return fail(HGM_ERR_EMPTY_POINT_SET, "no models");
+    std::vector<int32_t> first((size_t)n_models + 1, 0);
+    for (int c = 0; c < n_chains; ++c) {
+        if (chain_model[c] < 0 || chain_model[c] >= n_models) return fail(HGM_ERR_INVALID_ARGUMENT, "chain_model out of range");
+        if (c > 0 && chain_model[c] < chain_model[c - 1])
+            return fail(HGM_ERR_INVALID_ARGUMENT, "chains must be grouped by model (chain_model non-decreasing)");
+        ++first[(size_t)chain_model[c] + 1];
+    }
+    for (int m = 0; m < n_models; ++m) {
+        if (first[(size_t)m + 1] == 0) return fail(HGM_ERR_EMPTY_POINT_SET, "a model has no chain");
+        first[(size_t)m + 1] += first[(size_t)m];
+    }
+    const int count = offsets->count;
+    if (count == 0) return HGM_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    HGM_CUDA(cudaSetDevice(scene->device));
+    DevBuf Eb, Ab, Sb, fb;
+    HGM_TRY(Eb.alloc(sizeof(float) * (size_t)n_chains * count, s));
+    HGM_TRY(Ab.alloc(sizeof(float) * (size_t)n_chains * count, s));
+    HGM_TRY(detect_scores(chains, n_chains, scene, params, offsets, Eb.as<float>(), Ab.as<float>(), s));
+    const bool dSall = S_all && is_device_ptr(S_all);
+    if (!dSall) HGM_TRY(Sb.alloc(sizeof(float) * (size_t)n_models * count, s));
+    float *Sd = dSall ? S_all : Sb.as<float>();
+    HGM_TRY(fb.alloc(sizeof(int32_t) * first.size(), s));
+    HGM_CUDA(cudaMemcpyAsync(fb.p, first.data(), sizeof(int32_t) * first.size(), cudaMemcpyHostToDevice, s));
+    HGM_TRY(chain_mean(score_mode == 0 ? Eb.as<float>() : Ab.as<float>(), n_chains, chain_model, fb.as<int32_t>(),
+                       n_models, count, Sd, s));
+    HGM_TRY(finish_detect(Sd, n_models, count, threshold, winner, score, S_all, dSall, s));
+    HGM_CUDA(cudaStreamSynchronize(s));  // `first` (host) must outlive its upload
     return HGM_OK;
 }
 

@@ -225,6 +225,30 @@ __global__ void k_offset_argmin(const float *__restrict__ score, int nm, int cou
     if (best) best[k] = v;
 }
 
+// Independent chains (f3, "Multiple points 2"): the distance of a model is
+// the average of its chains' scores.  S_model[m][k] = mean over chains c of model m
+// (chains grouped: chain_first[m] .. chain_first[m+1]) of S_chain[c][k], summed in
+// chain order.  One thread per (model, offset).
+__global__ void k_chain_mean(const float *__restrict__ S_chain, const int32_t *__restrict__ chain_first,
+                             int n_models, int count, float *__restrict__ S_model) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= (int64_t)n_models * count) return;
+    const int m = (int)(q / count), k = (int)(q % count);
+    const int c0 = chain_first[m], c1 = chain_first[m + 1];
+    float acc = 0.f;
+    for (int c = c0; c < c1; ++c) acc += S_chain[(int64_t)c * count + k];
+    S_model[q] = acc / (float)(c1 - c0);
+}
+
+hgm_status chain_mean(const float *S_chain, int n_chains, const int32_t *chain_model, const int32_t *chain_first,
+                      int n_models, int count, float *S_model, cudaStream_t s) {
+    (void)n_chains;
+    (void)chain_model;
+    const int64_t n = (int64_t)n_models * count;
+    if (n > 0) k_chain_mean<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(S_chain, chain_first, n_models, count, S_model);
+    return HGM_OK;
+}
+
 // Recognition vote (f1): block label = label of the block's winning prototype (-1 if
 // none); clip label = majority over labelled blocks, ties -> smallest label.  One CTA.
 __global__ void __launch_bounds__(256) k_block_vote(const int32_t *__restrict__ winner, int count,

@@ -122,7 +122,7 @@ bool profiling();
 
 // ------------------------------------------------------------------ launchers
 hgm_status scene_build_device(const hgm_points *dev_pts, int32_t T_max, cudaStream_t s, hgm_scene **out);
-hgm_status model_build_device(const hgm_points *dev_pts, cudaStream_t s, hgm_model **out);
+hgm_status model_build_device(const hgm_points *dev_pts, int rank, cudaStream_t s, hgm_model **out);
 
 // Unary table of a batch of NM models of M nodes each (model features stacked
 // model-major, node j = k*M + i), batched layout U[((i*nn) + (n - n_lo))*NM + k].
@@ -141,6 +141,8 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
                        cudaStream_t s);
 hgm_status offset_argmin(const float *score, int n_models, int count, float threshold, int32_t *winner,
                          float *best, cudaStream_t s);
+hgm_status chain_mean(const float *S_chain, int n_chains, const int32_t *chain_model, const int32_t *chain_first,
+                      int n_models, int count, float *S_model, cudaStream_t s);
 hgm_status block_vote(const int32_t *winner, int count, const int32_t *label, int n_labels, int32_t *block_label,
                       int32_t *clip_label, cudaStream_t s);
 

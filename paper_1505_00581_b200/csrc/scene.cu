@@ -247,17 +247,25 @@ hgm_status scene_build_device(const hgm_points *pts, int32_t T_max, cudaStream_t
 // input point of that frame; the max-saliency scan with a strict ">" keeps the
 // earliest one on ties (R-D1).
 __global__ void k_model_select(int64_t n, const int32_t *__restrict__ t, const int32_t *__restrict__ order,
-                               const float *__restrict__ sal, int32_t *sel, int32_t *M_out) {
-    // one thread: n is a model's point count (hundreds)
+                               const float *__restrict__ sal, int rank, int32_t *sel, int32_t *M_out) {
+    // one thread: n is a model's point count (hundreds).  Per frame, the point of
+    // saliency rank `rank` (0 = most salient; rank r = chain r of the
+    // independent-chains model); ties: earlier input point first
+    // (the frame sort is stable, so group position = input order).
     if (threadIdx.x == 0) {
         int m = 0;
         for (int64_t k = 0; k < n;) {
-            int64_t best = k, j = k + 1;
-            while (j < n && t[j] == t[k]) {
-                if (sal[order[j]] > sal[order[best]]) best = j;
-                ++j;
+            int64_t j = k + 1;
+            while (j < n && t[j] == t[k]) ++j;
+            for (int64_t q = k; q < j; ++q) {
+                int beaten = 0;
+                const float sq = sal[order[q]];
+                for (int64_t r = k; r < j; ++r) {
+                    const float sr = sal[order[r]];
+                    beaten += (sr > sq || (sr == sq && r < q)) ? 1 : 0;
+                }
+                if (beaten == rank) sel[m++] = (int32_t)q;
             }
-            sel[m++] = (int32_t)best;
             k = j;
         }
         *M_out = m;
@@ -302,7 +310,7 @@ __global__ void k_model_steps(int M, const int32_t *__restrict__ t, const float 
     step[i] = make_float4((float)(t[c] - t[b]), (float)(t[b] - t[a]), A1, K2);
 }
 
-hgm_status model_build_device(const hgm_points *pts, cudaStream_t s, hgm_model **out) {
+hgm_status model_build_device(const hgm_points *pts, int rank, cudaStream_t s, hgm_model **out) {
     const int64_t n = pts->n;
     if (n > 1000000) return fail(HGM_ERR_INVALID_ARGUMENT, "model point set too large");
     Timer tm(s, K_MODEL);
@@ -312,14 +320,15 @@ hgm_status model_build_device(const hgm_points *pts, cudaStream_t s, hgm_model *
     HGM_TRY(sel.alloc(sizeof(int32_t) * n, s));
     HGM_TRY(Mdev.alloc(sizeof(int32_t), s));
     HGM_TRY(sort_by_frame(pts->frame, n, keys.as<int32_t>(), order.as<int32_t>(), s));
-    k_model_select<<<1, 32, 0, s>>>(n, keys.as<int32_t>(), order.as<int32_t>(), pts->saliency, sel.as<int32_t>(),
-                                    Mdev.as<int32_t>());
+    k_model_select<<<1, 32, 0, s>>>(n, keys.as<int32_t>(), order.as<int32_t>(), pts->saliency, rank,
+                                    sel.as<int32_t>(), Mdev.as<int32_t>());
     count_launch(K_MODEL);
     int32_t M = 0, t0 = 0;
     HGM_CUDA(cudaMemcpyAsync(&M, Mdev.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     HGM_CUDA(cudaMemcpyAsync(&t0, keys.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     HGM_CUDA(cudaStreamSynchronize(s));
     if (t0 < 0) return fail(HGM_ERR_INVALID_ARGUMENT, "negative frame index");
+    if (M == 0) return fail(HGM_ERR_EMPTY_POINT_SET, "no frame has a point of this saliency rank");
     hgm_model *m = new hgm_model();
     HGM_CUDA(cudaGetDevice(&m->device));
     m->M = M;

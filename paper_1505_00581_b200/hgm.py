@@ -20,7 +20,7 @@ LIB_PATH = os.environ.get("HGM_LIB") or os.path.join(_HERE, "lib", "libhgm.so") 
 STATUS = {0: "HGM_OK", 1: "HGM_ERR_EMPTY_POINT_SET", 2: "HGM_ERR_DIMENSION_MISMATCH",
           3: "HGM_ERR_INVALID_ARGUMENT", 4: "HGM_ERR_OUT_OF_MEMORY", 5: "HGM_ERR_CUDA"}
 
-EXPORTS = ("hgm_build_model_graph", "hgm_build_model_graph_dev", "hgm_model_num_nodes", "hgm_free_model",
+EXPORTS = ("hgm_build_model_graph", "hgm_build_model_graph_dev", "hgm_build_model_chain", "hgm_detect_chains", "hgm_model_num_nodes", "hgm_free_model",
            "hgm_build_scene_index", "hgm_build_scene_index_dev", "hgm_scene_num_nodes", "hgm_free_scene",
            "hgm_match_model_at_offsets", "hgm_detect_actions", "hgm_classify_blocks", "hgm_set_profiling", "hgm_get_stats",
            "hgm_last_error", "hgm_version")
@@ -68,6 +68,9 @@ def lib():
         L = C.CDLL(LIB_PATH)
         vp, P = C.c_void_p, C.POINTER
         L.hgm_build_model_graph.argtypes = [P(_Points), C.c_int, P(vp)]
+        L.hgm_build_model_chain.argtypes = [P(_Points), C.c_int, C.c_int32, P(vp)]
+        L.hgm_detect_chains.argtypes = [P(vp), C.c_int32, vp, C.c_int32, vp, P(Params), P(Offsets), C.c_int32,
+                                        C.c_float, vp, vp, vp, vp]
         L.hgm_build_model_graph_dev.argtypes = [P(_Points), vp, P(vp)]
         L.hgm_model_num_nodes.argtypes = [vp, P(C.c_int32)]
         L.hgm_free_model.argtypes = [vp]
@@ -212,6 +215,22 @@ def build_model_graph(points, device: int = 0, stream=None) -> Model:
     return Model(out.value)
 
 
+def build_model_chains(points, n_chains: int, device: int = 0) -> list:
+    """Chains 0..n_chains-1 of the independent-chains model:
+    chain r keeps each frame's point of saliency rank r.  Ranks no frame reaches
+    are skipped (the list may be shorter than n_chains)."""
+    hp = _HostPoints(points)
+    out = []
+    for r in range(int(n_chains)):
+        h = C.c_void_p()
+        st = lib().hgm_build_model_chain(C.byref(hp.s), int(device), int(r), C.byref(h))
+        if st == 1:  # HGM_ERR_EMPTY_POINT_SET: no frame has more than r points
+            break
+        _check(st)
+        out.append(Model(h.value))
+    return out
+
+
 def build_scene_index(points, device: int = 0, T_max: int = 10, stream=None) -> Scene:
     """Scene index."""
     out = C.c_void_p()
@@ -286,6 +305,34 @@ def detect_actions(models, scene: Scene, params=None, first_frame=0, stride=1, c
     _check(lib().hgm_detect_actions(handles, nm, scene.h, C.byref(_params(params)), C.byref(o), int(score_mode),
                                     float(threshold), _ptr(winner), _ptr(score), _ptr(E_all), _stream_ptr(stream)))
     return DetectResult(winner, score, E_all)
+
+
+def detect_chains(chains, chain_model, n_models, scene: Scene, params=None, first_frame=0, stride=1, count=1,
+                  window=60, score_mode=0, threshold=math.inf, want_S_all=False, device_out=True,
+                  stream=None) -> DetectResult:
+    """Detection with multi-chain models (hgm_detect_chains): a
+    model's distance is the mean of its chains' scores.  `E_all` of the result holds
+    the per-model means when want_S_all."""
+    nc = len(chains)
+    cm = np.ascontiguousarray(chain_model, dtype=np.int32)
+    if cm.shape != (nc,):
+        raise ValueError("chain_model must have one entry per chain")
+    if device_out:
+        import torch
+
+        winner = torch.empty(count, dtype=torch.int32, device="cuda")
+        score = torch.empty(count, dtype=torch.float32, device="cuda")
+        S_all = torch.empty((n_models, count), dtype=torch.float32, device="cuda") if want_S_all else None
+    else:
+        winner = np.empty(count, np.int32)
+        score = np.empty(count, np.float32)
+        S_all = np.empty((n_models, count), np.float32) if want_S_all else None
+    handles = (C.c_void_p * nc)(*[m.h.value for m in chains])
+    o = Offsets(int(first_frame), int(stride), int(count), int(window))
+    _check(lib().hgm_detect_chains(handles, nc, cm.ctypes.data, int(n_models), scene.h, C.byref(_params(params)),
+                                   C.byref(o), int(score_mode), float(threshold), _ptr(winner), _ptr(score),
+                                   _ptr(S_all), _stream_ptr(stream)))
+    return DetectResult(winner, score, S_all)
 
 
 @dataclass

@@ -386,3 +386,42 @@ def test_single_instance_unpruned_full_size_properties(hgm):
         Ez = oracle.energy(chk.models[0], win, p, zl)
         assert abs(Ez - Es[-1]) <= tol(Ez), (T, Ez, Es[-1])
     assert Es[2] <= Es[1] + tol(Es[1]) and Es[1] <= Es[0] + tol(Es[0]), Es
+
+
+@pytest.mark.parametrize("score_mode", [0, 1])
+def test_detect_chains_matches_oracle(hgm, score_mode):
+    """f3 independent chains: 6 models of 2 points per frame -> 2 chains each, a C2 clip,
+    30 offsets; per-model mean scores and winners against oracle.detect_chains."""
+    wl = synth.make_workload("C2")
+    p = wl.params()
+    clip, count, stride = 7, 30, 18
+    w_o, s_o, S_o, cm_o = oracle.detect_chains(wl.models, 2, wl.scenes[clip], p, 0, stride, count, 60,
+                                               score_mode=score_mode)
+    scene = hgm.build_scene_index(wl.scenes[clip], device=0, T_max=10)
+    chains, cm = [], []
+    for m, pts in enumerate(wl.models):
+        ch = hgm.build_model_chains(pts, 2, device=0)
+        for r, c in enumerate(ch):
+            assert c.M == len(oracle.model_chain_rank(pts.frame, pts.saliency, r))
+        chains += ch
+        cm += [m] * len(ch)
+    assert cm == cm_o.tolist()
+    det = hgm.detect_chains(chains, cm, len(wl.models), scene, p, 0, stride, count, 60, score_mode=score_mode,
+                            want_S_all=True, device_out=False)
+    assert np.all(np.abs(det.E_all - S_o) <= 2 * tol(S_o)), np.max(np.abs(det.E_all - S_o))
+    for k in range(count):
+        w = int(det.winner[k])
+        if w != int(w_o[k]):
+            assert abs(S_o[w, k] - S_o[w_o[k], k]) <= 2 * tol(S_o[w_o[k], k]), k
+        assert abs(float(det.score[k]) - s_o[k]) <= 2 * tol(s_o[k])
+
+
+def test_chain_builder_errors(hgm):
+    wl = synth.make_workload("C1")
+    ch = hgm.build_model_chains(wl.models[0], 5, device=0)
+    assert len(ch) == 2  # C1's model has 2 points in every occupied frame
+    scene = hgm.build_scene_index(wl.scenes[0], device=0, T_max=10)
+    with pytest.raises(hgm.HGMError):  # chains not grouped by model
+        hgm.detect_chains(ch, [1, 0], 2, scene, wl.params(), 0, 1, 4, 60)
+    with pytest.raises(hgm.HGMError):  # model 1 has no chain
+        hgm.detect_chains(ch, [0, 0], 2, scene, wl.params(), 0, 1, 4, 60)
