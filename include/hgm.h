@@ -137,6 +137,29 @@ hgm_status hgm_detect_chains(const hgm_model *const *chains, int32_t n_chains, c
                              const hgm_offsets *offsets, int32_t score_mode, float threshold, int32_t *winner,
                              float *score, float *S_all, void *stream);
 
+/* Streaming detection (P:L739-743 continuous processing in
+ * overlapping blocks).  A stream owns a host copy of the points of the frames its
+ * future windows still need; the models are borrowed (they must outlive the stream).
+ * hgm_stream_create: window W, stride, score_mode and threshold as hgm_detect_actions;
+ *   offsets are 0, stride, 2*stride, ... of the stream's frame clock (starting at 0).
+ * hgm_stream_push: appends `pts` (host arrays; every frame in [seen, seen + n_frames),
+ *   `seen` = frames pushed before; pts may be NULL or empty) and advances the clock by
+ *   n_frames; then detects every offset o not yet reported whose window is complete
+ *   (o + W <= seen), writing *n_out results (winner / score as hgm_detect_actions, host
+ *   or device, capacity entries available) for offsets *first_offset + j * stride.
+ *   Results are identical to one hgm_detect_actions call over the whole stream.
+ *   Synchronous.  Errors: NULL st / n_out / first_offset, n_frames < 0, points outside
+ *   the pushed frames, capacity too small -> INVALID_ARGUMENT; F differing from the
+ *   models' -> DIMENSION_MISMATCH; windows to report but no point retained at all ->
+ *   EMPTY_POINT_SET; CUDA errors as elsewhere. */
+typedef struct hgm_stream hgm_stream;
+hgm_status hgm_stream_create(const hgm_model *const *models, int32_t n_models, const hgm_params *params,
+                             int32_t window, int32_t stride, int32_t score_mode, float threshold, int32_t device,
+                             hgm_stream **out);
+hgm_status hgm_stream_push(hgm_stream *stream, const hgm_points *pts, int32_t n_frames, int32_t capacity,
+                           int32_t *winner, float *score, int32_t *n_out, int64_t *first_offset);
+void hgm_stream_free(hgm_stream *stream);
+
 /* Recognition ("nearest prototype classifier (NPC)" with the
  * appearance distance only, P:L739-743 blocks of 60 frames; SPEC classify / split_blocks):
  * every prototype is matched against every block (block k = frames

@@ -1,0 +1,122 @@
+// Streaming detection ("If the scene video is cut
+// into smaller blocks of 60 frames, which is necessary for continuous video
+// processing, real time performance can be achieved ... Additional processing will be
+// required in order to treat overlapping blocks").
+//
+// Frames arrive in order.  After each push, every offset whose window [o, o + W) is
+// complete (o + W <= frames pushed) and not yet reported is detected, exactly as a
+// one-shot hgm_detect_actions over the whole stream would (same windows, same kernels):
+// the stream keeps only the points of frames >= the next unreported offset, rebases
+// their frames to it (every quantity of the method depends on frame differences only),
+// builds a scene index of them and runs the detect path on the completed offsets.
+#include <vector>
+
+#include "hgm_internal.cuh"
+
+struct hgm_stream {
+    std::vector<const hgm_model *> models;
+    hgm_params params{};
+    int32_t window = 60, stride = 1, score_mode = 0, device = 0, F = 0;
+    float threshold = 0.f;
+    int64_t seen = 0;    // frames pushed so far
+    int64_t o_next = 0;  // next unreported offset (a multiple of stride)
+    // retained points (host), absolute frames >= o_next
+    std::vector<int32_t> frame;
+    std::vector<float> x, y, sal, feat;
+};
+
+using namespace hgm;
+
+extern "C" {
+
+hgm_status hgm_stream_create(const hgm_model *const *models, int32_t n_models, const hgm_params *params,
+                             int32_t window, int32_t stride, int32_t score_mode, float threshold, int32_t device,
+                             hgm_stream **out) {
+    if (!out || !params) return fail(HGM_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (!models || n_models <= 0) return fail(HGM_ERR_EMPTY_POINT_SET, "empty model dictionary");
+    if (window < 1 || stride < 1) return fail(HGM_ERR_INVALID_ARGUMENT, "window and stride must be >= 1");
+    if (score_mode != 0 && score_mode != 1) return fail(HGM_ERR_INVALID_ARGUMENT, "score_mode must be 0 or 1");
+    if (params->T < 1) return fail(HGM_ERR_INVALID_ARGUMENT, "T < 1");
+    auto *st = new hgm_stream();
+    for (int m = 0; m < n_models; ++m) {
+        if (!models[m]) {
+            delete st;
+            return fail(HGM_ERR_INVALID_ARGUMENT, "NULL model handle");
+        }
+        st->models.push_back(models[m]);
+    }
+    st->F = models[0]->F;
+    st->params = *params;
+    st->window = window;
+    st->stride = stride;
+    st->score_mode = score_mode;
+    st->threshold = threshold;
+    st->device = device;
+    *out = st;
+    return HGM_OK;
+}
+
+hgm_status hgm_stream_push(hgm_stream *st, const hgm_points *pts, int32_t n_frames, int32_t capacity,
+                           int32_t *winner, float *score, int32_t *n_out, int64_t *first_offset) {
+    if (!st || !n_out || !first_offset) return fail(HGM_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (n_frames < 0) return fail(HGM_ERR_INVALID_ARGUMENT, "n_frames < 0");
+    *n_out = 0;
+    *first_offset = st->o_next;
+    if (pts && pts->n > 0) {
+        if (!pts->frame || !pts->x || !pts->y || !pts->feat) return fail(HGM_ERR_INVALID_ARGUMENT, "NULL point array");
+        if (pts->F != st->F) return fail(HGM_ERR_DIMENSION_MISMATCH, "point and model descriptor lengths differ");
+        for (int64_t k = 0; k < pts->n; ++k)
+            if (pts->frame[k] < st->seen || pts->frame[k] >= st->seen + n_frames)
+                return fail(HGM_ERR_INVALID_ARGUMENT, "pushed point outside the pushed frames [seen, seen + n_frames)");
+        for (int64_t k = 0; k < pts->n; ++k) {
+            st->frame.push_back(pts->frame[k]);
+            st->x.push_back(pts->x[k]);
+            st->y.push_back(pts->y[k]);
+            st->sal.push_back(pts->saliency ? pts->saliency[k] : 0.f);
+        }
+        st->feat.insert(st->feat.end(), pts->feat, pts->feat + pts->n * (int64_t)st->F);
+    }
+    st->seen += n_frames;
+    if (st->seen < st->o_next + st->window) return HGM_OK;
+    const int64_t count = (st->seen - st->window - st->o_next) / st->stride + 1;
+    if (count > capacity || (count > 0 && (!winner || !score)))
+        return fail(HGM_ERR_INVALID_ARGUMENT, "output capacity below the offsets this push completes");
+    const int64_t base = st->o_next;
+    const int64_t n = (int64_t)st->frame.size();
+    if (n == 0) return fail(HGM_ERR_EMPTY_POINT_SET, "no retained point: every completed window is empty");
+    std::vector<int32_t> rf((size_t)n);
+    for (int64_t k = 0; k < n; ++k) rf[(size_t)k] = (int32_t)(st->frame[(size_t)k] - base);
+    hgm_points hp{n, st->F, rf.data(), st->x.data(), st->y.data(), st->sal.data(), st->feat.data(), nullptr};
+    hgm_scene *scene = nullptr;
+    HGM_TRY(hgm_build_scene_index(&hp, st->device, st->params.T, &scene));
+    hgm_offsets o{0, st->stride, (int32_t)count, st->window};
+    const hgm_status ds = hgm_detect_actions(st->models.data(), (int32_t)st->models.size(), scene, &st->params, &o,
+                                             st->score_mode, st->threshold, winner, score, nullptr, nullptr);
+    hgm_free_scene(scene);
+    HGM_TRY(ds);
+    HGM_CUDA(cudaStreamSynchronize(nullptr));
+    *n_out = (int32_t)count;
+    st->o_next += count * st->stride;
+    // drop the points no later window reads (frames < o_next)
+    int64_t w = 0;
+    for (int64_t k = 0; k < n; ++k) {
+        if (st->frame[(size_t)k] < st->o_next) continue;
+        st->frame[(size_t)w] = st->frame[(size_t)k];
+        st->x[(size_t)w] = st->x[(size_t)k];
+        st->y[(size_t)w] = st->y[(size_t)k];
+        st->sal[(size_t)w] = st->sal[(size_t)k];
+        if (w != k)
+            std::copy(st->feat.begin() + k * st->F, st->feat.begin() + (k + 1) * st->F, st->feat.begin() + w * st->F);
+        ++w;
+    }
+    st->frame.resize((size_t)w);
+    st->x.resize((size_t)w);
+    st->y.resize((size_t)w);
+    st->sal.resize((size_t)w);
+    st->feat.resize((size_t)(w * st->F));
+    return HGM_OK;
+}
+
+void hgm_stream_free(hgm_stream *st) { delete st; }
+
+}  // extern "C"

@@ -20,7 +20,7 @@ LIB_PATH = os.environ.get("HGM_LIB") or os.path.join(_HERE, "lib", "libhgm.so") 
 STATUS = {0: "HGM_OK", 1: "HGM_ERR_EMPTY_POINT_SET", 2: "HGM_ERR_DIMENSION_MISMATCH",
           3: "HGM_ERR_INVALID_ARGUMENT", 4: "HGM_ERR_OUT_OF_MEMORY", 5: "HGM_ERR_CUDA"}
 
-EXPORTS = ("hgm_build_model_graph", "hgm_build_model_graph_dev", "hgm_build_model_chain", "hgm_detect_chains", "hgm_model_num_nodes", "hgm_free_model",
+EXPORTS = ("hgm_stream_create", "hgm_stream_push", "hgm_stream_free", "hgm_build_model_graph", "hgm_build_model_graph_dev", "hgm_build_model_chain", "hgm_detect_chains", "hgm_model_num_nodes", "hgm_free_model",
            "hgm_build_scene_index", "hgm_build_scene_index_dev", "hgm_scene_num_nodes", "hgm_free_scene",
            "hgm_match_model_at_offsets", "hgm_detect_actions", "hgm_classify_blocks", "hgm_set_profiling", "hgm_get_stats",
            "hgm_last_error", "hgm_version")
@@ -68,6 +68,11 @@ def lib():
         L = C.CDLL(LIB_PATH)
         vp, P = C.c_void_p, C.POINTER
         L.hgm_build_model_graph.argtypes = [P(_Points), C.c_int, P(vp)]
+        L.hgm_stream_create.argtypes = [P(vp), C.c_int32, P(Params), C.c_int32, C.c_int32, C.c_int32, C.c_float,
+                                        C.c_int32, P(vp)]
+        L.hgm_stream_push.argtypes = [vp, P(_Points), C.c_int32, C.c_int32, vp, vp, P(C.c_int32), P(C.c_int64)]
+        L.hgm_stream_free.argtypes = [vp]
+        L.hgm_stream_free.restype = None
         L.hgm_build_model_chain.argtypes = [P(_Points), C.c_int, C.c_int32, P(vp)]
         L.hgm_detect_chains.argtypes = [P(vp), C.c_int32, vp, C.c_int32, vp, P(Params), P(Offsets), C.c_int32,
                                         C.c_float, vp, vp, vp, vp]
@@ -333,6 +338,38 @@ def detect_chains(chains, chain_model, n_models, scene: Scene, params=None, firs
                                    C.byref(o), int(score_mode), float(threshold), _ptr(winner), _ptr(score),
                                    _ptr(S_all), _stream_ptr(stream)))
     return DetectResult(winner, score, S_all)
+
+
+class Stream:
+    """Streaming detection (hgm_stream_*): push frames in order,
+    get the offsets whose windows completed.  The models must outlive the stream."""
+
+    def __init__(self, models, params=None, window=60, stride=1, score_mode=0, threshold=math.inf, device=0):
+        self.models = list(models)  # keep the handles alive
+        h = C.c_void_p()
+        handles = (C.c_void_p * len(self.models))(*[m.h.value for m in self.models])
+        _check(lib().hgm_stream_create(handles, len(self.models), C.byref(_params(params)), int(window), int(stride),
+                                       int(score_mode), float(threshold), int(device), C.byref(h)))
+        self.h = h
+        self.window, self.stride = int(window), int(stride)
+
+    def push(self, points, n_frames: int):
+        """Append `points` (frames in [seen, seen + n_frames), or None) and return
+        (first_offset, winner int32[n], score float32[n]) for the completed offsets."""
+        cap = int(n_frames) // self.stride + 2
+        winner = np.empty(cap, np.int32)
+        score = np.empty(cap, np.float32)
+        n = C.c_int32()
+        first = C.c_int64()
+        hp = _HostPoints(points) if points is not None and points.n > 0 else None
+        _check(lib().hgm_stream_push(self.h, C.byref(hp.s) if hp else None, int(n_frames), cap, winner.ctypes.data,
+                                     score.ctypes.data, C.byref(n), C.byref(first)))
+        return int(first.value), winner[: n.value].copy(), score[: n.value].copy()
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.h.value and _lib is not None:
+            _lib.hgm_stream_free(self.h)
+            self.h = None
 
 
 @dataclass

@@ -425,3 +425,46 @@ def test_chain_builder_errors(hgm):
         hgm.detect_chains(ch, [1, 0], 2, scene, wl.params(), 0, 1, 4, 60)
     with pytest.raises(hgm.HGMError):  # model 1 has no chain
         hgm.detect_chains(ch, [0, 0], 2, scene, wl.params(), 0, 1, 4, 60)
+
+
+@pytest.mark.parametrize("cfg,hop,stride", [("C1", 1, 1), ("C1", 7, 1), ("C1", 60, 5), ("C2", 250, 1),
+                                            ("C2", 33, 3)])
+def test_stream_equals_one_shot_detect(hgm, cfg, hop, stride):
+    """f4 streaming: pushing the scene `hop` frames at a time reports every offset once,
+    in order, bit-identical to one detect_actions call over the whole scene."""
+    wl = synth.make_workload(cfg)
+    sc_pts = wl.scenes[0]
+    p = wl.params()
+    nf = int(sc_pts.frame.max()) + 1
+    count = (nf - 60) // stride + 1
+    models = [hgm.build_model_graph(m, device=0) for m in wl.models]
+    scene = hgm.build_scene_index(sc_pts, device=0, T_max=p["T"])
+    ref = hgm.detect_actions(models, scene, p, 0, stride, count, 60, device_out=False)
+    st = hgm.Stream(models, p, window=60, stride=stride)
+    ws, ss, nxt = [], [], 0
+    for f0 in range(0, nf, hop):
+        n = min(hop, nf - f0)
+        sel = np.nonzero((sc_pts.frame >= f0) & (sc_pts.frame < f0 + n))[0]
+        first, w, s = st.push(sc_pts.take(sel), n)
+        if len(w):
+            assert first == nxt * stride
+            nxt += len(w)
+        ws.append(w)
+        ss.append(s)
+    w, s = np.concatenate(ws), np.concatenate(ss)
+    assert len(w) == count
+    assert np.array_equal(w, ref.winner) and np.array_equal(s, ref.score)
+    if cfg == "C1" and hop == 7:  # and against the oracle on the first offsets
+        r = oracle.detect(wl.models, sc_pts, p, 0, stride, 25, 60)
+        assert np.all(np.abs(s[:25] - r.score) <= 1e-6 + 1e-5 * np.abs(r.score))
+
+
+def test_stream_errors(hgm):
+    wl = synth.make_workload("C1")
+    models = [hgm.build_model_graph(wl.models[0], device=0)]
+    st = hgm.Stream(models, wl.params(), window=60, stride=1)
+    sc = wl.scenes[0]
+    with pytest.raises(hgm.HGMError):  # frames beyond the pushed range
+        st.push(sc.take(np.nonzero(sc.frame < 20)[0]), 10)
+    first, w, s = st.push(None, 59)  # nothing complete yet
+    assert len(w) == 0
