@@ -22,15 +22,18 @@ constexpr int KU_TJ = 8;    // model nodes per register tile
 
 __global__ void __launch_bounds__(KU_TN) k_unary(const float *__restrict__ mfeat, int M, int NM, int Fp,
                                                  const float *__restrict__ sfeat, int64_t n_lo, int64_t nn,
-                                                 float *__restrict__ U) {
+                                                 int tiles_per_y, float *__restrict__ U) {
     const int M_total = M * NM;
+    // blockIdx.y owns model-node tiles [y * tiles_per_y, (y + 1) * tiles_per_y): small
+    // scenes (few scene tiles) still fill the GPU
+    const int j_begin = blockIdx.y * tiles_per_y * KU_TJ, j_end = min(M_total, j_begin + tiles_per_y * KU_TJ);
     extern __shared__ float4 sm[];  // [KU_TJ][Fp/4] model descriptors
     const int F4 = Fp >> 2;
     const int64_t n = blockIdx.x * (int64_t)KU_TN + threadIdx.x;
     const bool live = n < nn;
     const float4 *srow = reinterpret_cast<const float4 *>(sfeat + (n_lo + (live ? n : 0)) * (int64_t)Fp);
-    for (int j0 = 0; j0 < M_total; j0 += KU_TJ) {
-        const int nj = min(KU_TJ, M_total - j0);
+    for (int j0 = j_begin; j0 < j_end; j0 += KU_TJ) {
+        const int nj = min(KU_TJ, j_end - j0);
         __syncthreads();
         for (int k = threadIdx.x; k < nj * F4; k += KU_TN)
             sm[k] = reinterpret_cast<const float4 *>(mfeat + (int64_t)j0 * Fp)[k];
@@ -72,7 +75,11 @@ hgm_status unary_table(const float *mfeat, int M, int NM, int Fp, const hgm_scen
     Timer tm(s, K_UNARY);
     const size_t smem = sizeof(float) * KU_TJ * Fp;
     if (smem > 48 * 1024) HGM_CUDA(cudaFuncSetAttribute(k_unary, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_unary<<<(unsigned)((nn + KU_TN - 1) / KU_TN), KU_TN, smem, s>>>(mfeat, M, NM, Fp, sc->feat, n_lo, nn, U);
+    const int64_t gx = (nn + KU_TN - 1) / KU_TN;
+    const int jt = (M * NM + KU_TJ - 1) / KU_TJ;                              // model-node tiles
+    const int gy_want = (int)std::min<int64_t>(jt, std::max<int64_t>(1, (4 * 148 + gx - 1) / gx));
+    const int tpy = (jt + gy_want - 1) / gy_want, gy = (jt + tpy - 1) / tpy;
+    k_unary<<<dim3((unsigned)gx, (unsigned)gy), KU_TN, smem, s>>>(mfeat, M, NM, Fp, sc->feat, n_lo, nn, tpy, U);
     count_launch(K_UNARY);
     HGM_CUDA(cudaGetLastError());
     return HGM_OK;
