@@ -30,34 +30,24 @@ __device__ __forceinline__ Best shfl_best(const Best &b, int o) {
                 __shfl_xor_sync(0xffffffffu, b.z2, o)};
 }
 
-// One CTA per window, one warp per model of the batch (blockDim = 32 * NM).
-// Eq. 13 init search: every (z1, z2) of the window -- real pairs are the window's
-// band entries (slot e of the alpha_3 layer), then (z1, eps), (eps, z2), (eps, eps) --
-// is scored for all NM models by all threads (each slot's NM values are one load of
-// the layer's state slot); block-wide lexicographic minimum per model.  Eq. 12
-// backtrack: warp k follows model k.
+// Eq. 13 init search (all models at once) over the slice q = q0, q0 + qs, ... of the
+// window's (z1, z2) list -- real pairs are the window's band entries (slot e of the
+// alpha_3 layer), then (z1, eps), (eps, z2), (eps, eps) -- each slot's NM values one
+// load of the layer's state slot; lexicographic minimum per model over the CTA into
+// s_best[k][0] (all threads may read it after the call).
 template <int NM>
-__global__ void __launch_bounds__(256) k_backtrack(SceneView sc, const InstDesc *__restrict__ inst,
-                                                   const float *__restrict__ hist, int64_t L, BTArgs bt,
-                                                   DPParams p) {
-    __shared__ Best s_best[NM][8];
+__device__ __forceinline__ void init_search(const SceneView &sc, const InstDesc &d, const float *__restrict__ hist,
+                                            int64_t L, const BTArgs &bt, const DPParams &p, int q0, int qs,
+                                            Best (*s_best)[8]) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
-    const InstDesc d = inst[blockIdx.x];
     const int Sw = d.we - d.wb, M = bt.M, T = p.T, SS = bt.SS;
-    const int EPSL = d.we;  // dummy label: orders after every real node (R11)
+    const int EPSL = d.we;
     auto Uk = [&](int i, int n, int k) { return __ldg(bt.U + ((int64_t)i * bt.nn + (n - bt.n_lo)) * NM + k); };
-    auto layer = [&](int i) -> const float * {
-        return (i >= 2 && i <= M - 1) ? hist + (int64_t)(i - 2) * L + d.off : nullptr;
-    };
-    // layer layout (dp_common.cuh): pair state (later, earlier) at qpad[earlier] - ppad + column
-    auto atk = [&](const float *l, int s, int k) { return l ? __ldg(l + (int64_t)s * SS + k) : 0.f; };
-
-    // ---- Eq. 13 init search (all models at once)
     Best best[NM];
 #pragma unroll
     for (int k = 0; k < NM; ++k) best[k] = Best{INFINITY, 0x7fffffff, 0x7fffffff};
     if (M == 1) {
-        for (int c = d.wb + tid; c <= d.we; c += nthr) {
+        for (int c = d.wb + q0 + tid; c <= d.we; c += qs) {
 #pragma unroll
             for (int k = 0; k < NM; ++k) {
                 const Best x{c < d.we ? __fmul_rn(p.l1, Uk(0, c, k)) : p.l1W, c, 0};
@@ -65,9 +55,9 @@ __global__ void __launch_bounds__(256) k_backtrack(SceneView sc, const InstDesc 
             }
         }
     } else {
-        const float *a3 = layer(2);
+        const float *a3 = hist + d.off;  // layer i = 2
         const int npp = d.npp;
-        for (int q = tid; q < npp + 2 * Sw + 1; q += nthr) {
+        for (int q = q0 + tid; q < npp + 2 * Sw + 1; q += qs) {
             int z1 = EPSL, z2 = EPSL, slot;
             bool ok = true;
             if (q < npp) {  // real pair (z1 -> z2): band entry of row z1
@@ -93,7 +83,8 @@ __global__ void __launch_bounds__(256) k_backtrack(SceneView sc, const InstDesc 
             for (int k = 0; k < NM; ++k) {
                 const float u1 = z1 < EPSL ? __fmul_rn(p.l1, Uk(0, z1, k)) : p.l1W;
                 const float u2 = z2 < EPSL ? __fmul_rn(p.l1, Uk(1, z2, k)) : p.l1W;
-                const Best x{__fadd_rn(__fadd_rn(u1, u2), atk(a3, slot, k)), z1, z2};
+                const float a = M > 2 ? __ldg(a3 + (int64_t)slot * SS + k) : 0.f;
+                const Best x{__fadd_rn(__fadd_rn(u1, u2), a), z1, z2};
                 if (better(x, best[k])) best[k] = x;
             }
         }
@@ -108,11 +99,62 @@ __global__ void __launch_bounds__(256) k_backtrack(SceneView sc, const InstDesc 
         if (lane == 0) s_best[k][warp] = best[k];
     }
     __syncthreads();
+    if (tid < NM) {
+        Best b = s_best[tid][0];
+        for (int w2 = 1; w2 < (nthr >> 5); ++w2)
+            if (better(s_best[tid][w2], b)) b = s_best[tid][w2];
+        s_best[tid][0] = b;
+    }
+    __syncthreads();
+}
+
+// Init search split over gridDim.y CTAs per window (dense windows: one CTA would
+// serialise hundreds of thousands of pairs); partial minima -> part[(w * P + y) * NM + k].
+template <int NM>
+__global__ void __launch_bounds__(256) k_bt_init(SceneView sc, const InstDesc *__restrict__ inst,
+                                                 const float *__restrict__ hist, int64_t L, BTArgs bt, DPParams p,
+                                                 Best *__restrict__ part) {
+    __shared__ Best s_best[NM][8];
+    const InstDesc d = inst[blockIdx.x];
+    init_search<NM>(sc, d, hist, L, bt, p, blockIdx.y * blockDim.x, gridDim.y * blockDim.x, s_best);
+    if (threadIdx.x < NM) part[((int64_t)blockIdx.x * gridDim.y + blockIdx.y) * NM + threadIdx.x] = s_best[threadIdx.x][0];
+}
+
+// One CTA per window, one warp per model of the batch (blockDim = 32 * max(NM, 4)):
+// the init search (here, or its P partial minima from k_bt_init), then the Eq. 12
+// backtrack, warp k following model k.
+template <int NM>
+__global__ void __launch_bounds__(256) k_backtrack(SceneView sc, const InstDesc *__restrict__ inst,
+                                                   const float *__restrict__ hist, int64_t L, BTArgs bt,
+                                                   DPParams p, const Best *__restrict__ part, int P) {
+    __shared__ Best s_best[NM][8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const InstDesc d = inst[blockIdx.x];
+    const int Sw = d.we - d.wb, M = bt.M, T = p.T, SS = bt.SS;
+    const int EPSL = d.we;  // dummy label: orders after every real node (R11)
+    auto Uk = [&](int i, int n, int k) { return __ldg(bt.U + ((int64_t)i * bt.nn + (n - bt.n_lo)) * NM + k); };
+    auto layer = [&](int i) -> const float * {
+        return (i >= 2 && i <= M - 1) ? hist + (int64_t)(i - 2) * L + d.off : nullptr;
+    };
+    // layer layout (dp_common.cuh): pair state (later, earlier) at qpad[earlier] - ppad + column
+    auto atk = [&](const float *l, int s, int k) { return l ? __ldg(l + (int64_t)s * SS + k) : 0.f; };
+    if (P == 0) init_search<NM>(sc, d, hist, L, bt, p, 0, blockDim.x, s_best);
     if (warp >= NM) return;
     const int kk = warp;  // this warp's model
-    Best bst = s_best[kk][0];
-    for (int w2 = 1; w2 < (nthr >> 5); ++w2)
-        if (better(s_best[kk][w2], bst)) bst = s_best[kk][w2];
+    Best bst;
+    if (P == 0) {
+        bst = s_best[kk][0];
+    } else {  // partial minima of k_bt_init; the lexicographic order is total, so any split agrees
+        bst = Best{INFINITY, 0x7fffffff, 0x7fffffff};
+        for (int y = lane; y < P; y += 32) {
+            const Best x = part[((int64_t)blockIdx.x * P + y) * NM + kk];
+            if (better(x, bst)) bst = x;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const Best y = shfl_best(bst, o);
+            if (better(y, bst)) bst = y;
+        }
+    }
     auto U = [&](int i, int n) { return Uk(i, n, kk); };
     auto at = [&](const float *l, int s) { return atk(l, s, kk); };
     auto a_be = [&](const float *l, int b) { return at(l, d.ntail + (b - d.wb)); };
@@ -169,16 +211,32 @@ __global__ void __launch_bounds__(256) k_backtrack(SceneView sc, const InstDesc 
             }
             return msg_n(a_be(nx, c), p.l1, U(i, c));
         };
-        // minimum and first argmin (ascending c), one value per lane and 32-candidate chunk
+        // minimum and first argmin (ascending c): groups of 4 x 32 candidates, a lane's
+        // 4 evaluations independent (their loads overlap); per group the lane keeps its
+        // first minimum, the warp the smallest c attaining the group minimum, and a
+        // group replaces the running result only if strictly smaller -- the same
+        // first argmin as a candidate-by-candidate scan
         float R = INFINITY;
         int arg = -1;
-        for (int cb = c0; cb < c1; cb += 32) {
-            const int c = cb + lane;
-            const float v = c < c1 ? value(c) : INFINITY;
-            const float cm = warp_min(v);
-            if (cm < R) {  // strictly better chunk: its first lane attaining cm
+        for (int cb = c0; cb < c1; cb += 128) {
+            float v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int c = cb + 32 * u + lane;
+                v[u] = c < c1 ? value(c) : INFINITY;
+            }
+            float lv = v[0];
+            int lc = cb + lane;
+#pragma unroll
+            for (int u = 1; u < 4; ++u)
+                if (v[u] < lv) {
+                    lv = v[u];
+                    lc = cb + 32 * u + lane;
+                }
+            const float cm = warp_min(lv);
+            if (cm < R) {
                 R = cm;
-                arg = cb + __ffs(__ballot_sync(0xffffffffu, c < c1 && v == cm)) - 1;
+                arg = (int)__reduce_min_sync(0xffffffffu, lv == cm ? (unsigned)lc : 0xffffffffu);
             }
         }
         float eps;
@@ -207,8 +265,17 @@ hgm_status launch_backtrack_warp(const SceneView &v, const InstDesc *dinst, int 
                                  const BTArgs &bt, const DPParams &p, cudaStream_t s) {
     if (ninst <= 0) return HGM_OK;
     const int threads = 32 * std::max(bt.NM, 4);  // >= 4 warps for the init search
-#define HGM_BT_CASE(n) \
-    case n: k_backtrack<n><<<ninst, threads, 0, s>>>(v, dinst, hist, L, bt, p); break
+    // few windows per launch (dense chunks): split their init search over P CTAs each
+    const int P = ninst >= 296 ? 0 : std::min(64, (296 + ninst - 1) / ninst);
+    DevBuf part;
+    if (P > 0) HGM_TRY(part.alloc(sizeof(Best) * (size_t)ninst * P * bt.NM, s));
+    Best *pp = P > 0 ? static_cast<Best *>(part.p) : nullptr;
+    if (P > 0) count_launch(K_BT);  // the split init search (the caller counts k_backtrack)
+#define HGM_BT_CASE(n)                                                                          \
+    case n:                                                                                     \
+        if (P > 0) k_bt_init<n><<<dim3(ninst, P), 256, 0, s>>>(v, dinst, hist, L, bt, p, pp);     \
+        k_backtrack<n><<<ninst, threads, 0, s>>>(v, dinst, hist, L, bt, p, pp, P);              \
+        break
     switch (bt.NM) {
         HGM_BT_CASE(1);
         HGM_BT_CASE(2);
