@@ -80,3 +80,44 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "hgm_oracle" not in txt, f
+
+
+def test_widened_entry_points_validate_before_device_work(lib):
+    """f1/f3/f4 entry points reject bad arguments with a status before touching a GPU."""
+    import ctypes as C
+
+    from paper_1505_00581_b200 import hgm
+
+    p = hgm._params(None)
+    o = hgm.Offsets(0, 1, 4, 60)
+    vp = C.c_void_p
+    h = C.c_void_p()
+    # streams: window 0 / stride 0 / score_mode 2 -> INVALID_ARGUMENT; empty dictionary -> EMPTY_POINT_SET
+    fake = (vp * 1)(vp(1))
+    assert lib.hgm_stream_create(fake, 1, C.byref(p), 0, 1, 0, 1.0, 0, C.byref(h)) == 3
+    assert lib.hgm_stream_create(fake, 1, C.byref(p), 60, 0, 0, 1.0, 0, C.byref(h)) == 3
+    assert lib.hgm_stream_create(fake, 1, C.byref(p), 60, 1, 2, 1.0, 0, C.byref(h)) == 3
+    assert lib.hgm_stream_create(fake, 0, C.byref(p), 60, 1, 0, 1.0, 0, C.byref(h)) == 1
+    n = C.c_int32()
+    f0 = C.c_int64()
+    assert lib.hgm_stream_push(None, None, 1, 0, None, None, C.byref(n), C.byref(f0)) == 3
+    # recognition: no prototypes / NULL labels / n_labels out of range
+    lab = (C.c_int32 * 1)(0)
+    assert lib.hgm_classify_blocks(fake, 0, lab, 1, vp(1), C.byref(p), C.byref(o), 1.0, None, None, None,
+                                   None) == 1
+    assert lib.hgm_classify_blocks(fake, 1, None, 1, vp(1), C.byref(p), C.byref(o), 1.0, None, None, None,
+                                   None) == 3
+    assert lib.hgm_classify_blocks(fake, 1, lab, 0, vp(1), C.byref(p), C.byref(o), 1.0, None, None, None,
+                                   None) == 3
+    # chains: empty chain list, and a negative rank
+    assert lib.hgm_detect_chains(fake, 0, None, 1, vp(1), C.byref(p), C.byref(o), 0, 1.0, None, None, None,
+                                 None) == 1
+    fr = np.zeros(2, np.int32)
+    xs = np.zeros(2, np.float32)
+    ft = np.zeros((2, 4), np.float32)
+
+    class Pts:
+        frame, x, y, saliency, feat, id = fr, xs, xs, xs, ft, None
+
+    hp = hgm._HostPoints(Pts())
+    assert lib.hgm_build_model_chain(C.byref(hp.s), 0, -1, C.byref(h)) == 3
