@@ -186,9 +186,20 @@ static bool make_tiling(const hgm_scene *sc, const hgm_offsets &o, int T, int NM
                     for (int64_t G0 = F0 - T + 1; G0 < F1 && fits;) {
                         int64_t G1 = G0 + 1;
                         if (foot(F0, F1, G0, G1, book) > cap) fits = false;
-                        // <= 255 segments per item (k_item_prep's uint8 state -> segment map)
-                        while (G1 < F1 && (G1 + 1 - G0) * (F1 - F0) <= 255 && foot(F0, F1, G0, G1 + 1, book) <= cap)
-                            ++G1;
+                        // largest G1 <= F1 whose item fits: <= 255 segments (k_item_prep's uint8
+                        // state -> segment map) and the stage cap; both monotone in G1, so a
+                        // binary search finds what growing G1 one frame at a time would
+                        if (fits) {
+                            int64_t lo = G1, hi = F1;
+                            while (lo < hi) {
+                                const int64_t mid = (lo + hi + 1) / 2;
+                                if ((mid - G0) * (F1 - F0) <= 255 && foot(F0, F1, G0, mid, book) <= cap)
+                                    lo = mid;
+                                else
+                                    hi = mid - 1;
+                            }
+                            G1 = lo;
+                        }
                         account(F0, F1, G0, G1);
                         G0 = G1;
                     }
