@@ -669,19 +669,36 @@ __global__ void k_items(SceneView sc, const InstDesc *__restrict__ inst, int nin
                         const int32_t *__restrict__ gstart, const int32_t *__restrict__ tile_of, int tf_lo,
                         const int32_t *__restrict__ sub_begin, const int32_t *__restrict__ sub_g,
                         const int32_t *__restrict__ item_base, int base0, WorkItem *items) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    // one warp per window; lane j of a round takes b-tile g_first + round*32 + j (a window
+    // of the single-instance regime has hundreds of tiles and thousands of chunks)
+    const int k = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
     if (k >= ninst) return;
     const InstDesc d = inst[k];
     const int g_first = __ldg(tile_of + (d.o - tf_lo)), g_last = __ldg(tile_of + (d.o + W - 1 - tf_lo));
-    int idx = __ldg(item_base + k) - base0;
-    for (int gt = g_first; gt <= g_last; ++gt) {
+    int idx0 = __ldg(item_base + k) - base0;
+    for (int g0 = g_first; g0 <= g_last; g0 += 32) {
+        const int gt = g0 + lane;
+        const bool on = gt <= g_last;
+        int F0 = 0, F1 = 0, sb0 = 0, sb1 = 0, n = 0;
+        if (on) {
+            F0 = max(__ldg(gstart + gt), d.o);
+            F1 = min(__ldg(gstart + gt + 1), d.o + W);
+            sb0 = __ldg(sub_begin + gt);
+            sb1 = __ldg(sub_begin + gt + 1);
+            for (int sb = sb0; sb < sb1; ++sb)  // chunks meeting the window (the first always counts)
+                n += (sb == sb0 || max(__ldg(sub_g + 2 * sb), d.o) < min(__ldg(sub_g + 2 * sb + 1), F1)) ? 1 : 0;
+        }
+        const int incl = warp_incl_scan(n, lane);
+        int idx = idx0 + incl - n;
+        idx0 += __shfl_sync(0xffffffffu, incl, 31);
+        if (!on) continue;
         bool first_of_tile = true;
-        for (int sb = __ldg(sub_begin + gt); sb < __ldg(sub_begin + gt + 1); ++sb) {
+        for (int sb = sb0; sb < sb1; ++sb) {
             WorkItem w{};
             w.d = d;
             w.live = 1;
-            w.F0 = max(__ldg(gstart + gt), d.o);
-            w.F1 = min(__ldg(gstart + gt + 1), d.o + W);
+            w.F0 = F0;
+            w.F1 = F1;
             w.G0 = max(__ldg(sub_g + 2 * sb), d.o);
             w.G1 = min(__ldg(sub_g + 2 * sb + 1), w.F1);
             if (w.G0 >= w.G1 && !first_of_tile) continue;  // chunk entirely before the window
@@ -859,8 +876,8 @@ hgm_status launch_items(const SceneView &v, const InstDesc *dinst, int ninst, in
                         const int32_t *tile_of, int tf_lo, const int32_t *sub_begin, const int32_t *sub_g,
                         const int32_t *item_base, int base0, WorkItem *items, cudaStream_t s) {
     if (ninst > 0)
-        k_items<<<(ninst + 127) / 128, 128, 0, s>>>(v, dinst, ninst, W, T, gstart, tile_of, tf_lo, sub_begin, sub_g,
-                                                    item_base, base0, items);
+        k_items<<<(unsigned)((ninst + 3) / 4), 128, 0, s>>>(v, dinst, ninst, W, T, gstart, tile_of, tf_lo, sub_begin,
+                                                            sub_g, item_base, base0, items);
     return HGM_OK;
 }
 
