@@ -76,7 +76,8 @@ struct BookPlan {
             return r;
         };
         nst = take(16);
-        seg = take(sizeof(Seg) * (size_t)c.FT * (T - 1));
+        // <= 255 segments per item (the host tiling caps them: uint8 state -> segment map)
+        seg = take(sizeof(Seg) * (size_t)std::min(c.FT * (T - 1), 256));
         rows = take(sizeof(int) * NROWI * (size_t)c.NA);
         map = take((size_t)c.NST);
         total = o;
