@@ -150,8 +150,8 @@ hgm_status hgm_detect_chains(const hgm_model *const *chains, int32_t n_chains, c
  *   Results are identical to one hgm_detect_actions call over the whole stream.
  *   Synchronous.  Errors: NULL st / n_out / first_offset, n_frames < 0, points outside
  *   the pushed frames, capacity too small -> INVALID_ARGUMENT; F differing from the
- *   models' -> DIMENSION_MISMATCH; windows to report but no point retained at all ->
- *   EMPTY_POINT_SET; CUDA errors as elsewhere. */
+ *   models' -> DIMENSION_MISMATCH; CUDA errors as elsewhere.  Windows without points
+ *   (silent stretches) are valid and give the all-dummy result. */
 typedef struct hgm_stream hgm_stream;
 hgm_status hgm_stream_create(const hgm_model *const *models, int32_t n_models, const hgm_params *params,
                              int32_t window, int32_t stride, int32_t score_mode, float threshold, int32_t device,

@@ -6,9 +6,11 @@
 // Frames arrive in order.  After each push, every offset whose window [o, o + W) is
 // complete (o + W <= frames pushed) and not yet reported is detected, exactly as a
 // one-shot hgm_detect_actions over the whole stream would (same windows, same kernels):
-// the stream keeps only the points of frames >= the next unreported offset, rebases
-// their frames to it (every quantity of the method depends on frame differences only),
+// the stream keeps only the points of frames >= the next unreported offset o_next,
+// rebases their frames to o_next - 1 (every quantity of the method depends on frame
+// differences only), adds an anchor node at the rebased frame 0 (before every window),
 // builds a scene index of them and runs the detect path on the completed offsets.
+#include <algorithm>
 #include <vector>
 
 #include "hgm_internal.cuh"
@@ -81,15 +83,25 @@ hgm_status hgm_stream_push(hgm_stream *st, const hgm_points *pts, int32_t n_fram
     const int64_t count = (st->seen - st->window - st->o_next) / st->stride + 1;
     if (count > capacity || (count > 0 && (!winner || !score)))
         return fail(HGM_ERR_INVALID_ARGUMENT, "output capacity below the offsets this push completes");
-    const int64_t base = st->o_next;
-    const int64_t n = (int64_t)st->frame.size();
-    if (n == 0) return fail(HGM_ERR_EMPTY_POINT_SET, "no retained point: every completed window is empty");
-    std::vector<int32_t> rf((size_t)n);
-    for (int64_t k = 0; k < n; ++k) rf[(size_t)k] = (int32_t)(st->frame[(size_t)k] - base);
-    hgm_points hp{n, st->F, rf.data(), st->x.data(), st->y.data(), st->sal.data(), st->feat.data(), nullptr};
+    // frames rebased to base = o_next - 1; an anchor node at rebased frame 0 lies before
+    // every window [1 + k * stride, ...) so it is never a label (R13), and it keeps the
+    // point set non-empty through silent stretches (windows without points are valid)
+    const int64_t base = st->o_next - 1;
+    const int64_t n = (int64_t)st->frame.size(), F = st->F;
+    std::vector<int32_t> rf((size_t)n + 1);
+    std::vector<float> rx((size_t)n + 1), ry((size_t)n + 1), rs((size_t)n + 1), rfeat((size_t)((n + 1) * F));
+    rf[0] = 0;
+    rx[0] = ry[0] = rs[0] = 0.f;
+    std::fill(rfeat.begin(), rfeat.begin() + F, 0.f);
+    for (int64_t k = 0; k < n; ++k) rf[(size_t)k + 1] = (int32_t)(st->frame[(size_t)k] - base);
+    std::copy(st->x.begin(), st->x.end(), rx.begin() + 1);
+    std::copy(st->y.begin(), st->y.end(), ry.begin() + 1);
+    std::copy(st->sal.begin(), st->sal.end(), rs.begin() + 1);
+    std::copy(st->feat.begin(), st->feat.end(), rfeat.begin() + F);
+    hgm_points hp{n + 1, st->F, rf.data(), rx.data(), ry.data(), rs.data(), rfeat.data(), nullptr};
     hgm_scene *scene = nullptr;
     HGM_TRY(hgm_build_scene_index(&hp, st->device, st->params.T, &scene));
-    hgm_offsets o{0, st->stride, (int32_t)count, st->window};
+    hgm_offsets o{1, st->stride, (int32_t)count, st->window};
     const hgm_status ds = hgm_detect_actions(st->models.data(), (int32_t)st->models.size(), scene, &st->params, &o,
                                              st->score_mode, st->threshold, winner, score, nullptr, nullptr);
     hgm_free_scene(scene);

@@ -468,3 +468,30 @@ def test_stream_errors(hgm):
         st.push(sc.take(np.nonzero(sc.frame < 20)[0]), 10)
     first, w, s = st.push(None, 59)  # nothing complete yet
     assert len(w) == 0
+
+
+@pytest.mark.parametrize("gap", [(0, 75), (200, 380)])
+def test_stream_through_silent_stretches(hgm, gap):
+    """f4: frames without any point (at the start, or a 180-frame silence) give windows
+    with no node; the stream still equals one-shot detect on the same scene."""
+    wl = synth.make_workload("C1")
+    sc0 = wl.scenes[0]
+    sc_pts = sc0.take(np.nonzero((sc0.frame < gap[0]) | (sc0.frame >= gap[1]))[0])
+    p = wl.params()
+    nf = 600
+    count = nf - 60 + 1
+    models = [hgm.build_model_graph(m, device=0) for m in wl.models]
+    scene = hgm.build_scene_index(sc_pts, device=0, T_max=p["T"])
+    ref = hgm.detect_actions(models, scene, p, 0, 1, count, 60, device_out=False)
+    st = hgm.Stream(models, p, window=60, stride=1)
+    ws, ss = [], []
+    for f0 in range(0, nf, 25):
+        sel = np.nonzero((sc_pts.frame >= f0) & (sc_pts.frame < f0 + 25))[0]
+        _, w, s = st.push(sc_pts.take(sel), 25)
+        ws.append(w)
+        ss.append(s)
+    w, s = np.concatenate(ws), np.concatenate(ss)
+    assert np.array_equal(w, ref.winner) and np.array_equal(s, ref.score)
+    r = oracle.detect(wl.models, sc_pts, p, 0, 1, count, 60, pairs=[(0, k) for k in range(gap[0], gap[1] - 60 + 1, 17)])
+    for k in range(gap[0], gap[1] - 60 + 1, 17):  # empty windows: the all-dummy energy
+        assert abs(s[k] - r.E[0, k]) <= 1e-6 + 1e-5 * abs(r.E[0, k])
