@@ -525,8 +525,7 @@ hgm_status hgm_detect_chains(const hgm_model *const *chains, int32_t n_chains, c
     float *Sd = dSall ? S_all : Sb.as<float>();
     HGM_TRY(fb.alloc(sizeof(int32_t) * first.size(), s));
     HGM_CUDA(cudaMemcpyAsync(fb.p, first.data(), sizeof(int32_t) * first.size(), cudaMemcpyHostToDevice, s));
-    HGM_TRY(chain_mean(score_mode == 0 ? Eb.as<float>() : Ab.as<float>(), n_chains, chain_model, fb.as<int32_t>(),
-                       n_models, count, Sd, s));
+    HGM_TRY(chain_mean(score_mode == 0 ? Eb.as<float>() : Ab.as<float>(), fb.as<int32_t>(), n_models, count, Sd, s));
     HGM_TRY(finish_detect(Sd, n_models, count, threshold, winner, score, S_all, dSall, s));
     HGM_CUDA(cudaStreamSynchronize(s));  // `first` (host) must outlive its upload
     return HGM_OK;

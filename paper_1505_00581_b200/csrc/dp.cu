@@ -240,10 +240,8 @@ __global__ void k_chain_mean(const float *__restrict__ S_chain, const int32_t *_
     S_model[q] = acc / (float)(c1 - c0);
 }
 
-hgm_status chain_mean(const float *S_chain, int n_chains, const int32_t *chain_model, const int32_t *chain_first,
-                      int n_models, int count, float *S_model, cudaStream_t s) {
-    (void)n_chains;
-    (void)chain_model;
+hgm_status chain_mean(const float *S_chain, const int32_t *chain_first, int n_models, int count, float *S_model,
+                      cudaStream_t s) {
     const int64_t n = (int64_t)n_models * count;
     if (n > 0) k_chain_mean<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(S_chain, chain_first, n_models, count, S_model);
     return HGM_OK;

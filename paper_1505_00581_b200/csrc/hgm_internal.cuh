@@ -141,8 +141,8 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
                        cudaStream_t s);
 hgm_status offset_argmin(const float *score, int n_models, int count, float threshold, int32_t *winner,
                          float *best, cudaStream_t s);
-hgm_status chain_mean(const float *S_chain, int n_chains, const int32_t *chain_model, const int32_t *chain_first,
-                      int n_models, int count, float *S_model, cudaStream_t s);
+hgm_status chain_mean(const float *S_chain, const int32_t *chain_first, int n_models, int count, float *S_model,
+                      cudaStream_t s);
 hgm_status block_vote(const int32_t *winner, int count, const int32_t *label, int n_labels, int32_t *block_label,
                       int32_t *clip_label, cudaStream_t s);
 
