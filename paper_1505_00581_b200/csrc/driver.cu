@@ -143,7 +143,15 @@ static bool make_tiling(const hgm_scene *sc, const hgm_offsets &o, int T, int NM
     size_t budgets[3] = {(size_t)(benv ? atoi(benv) : 110) * 1024, 220 * 1024, 220 * 1024};
     if (const char *menv = getenv("HGM_SMEM_MAX_KB"))  // testing: cap every budget (forces the fallbacks)
         for (size_t &b : budgets) b = std::min(b, (size_t)atoi(menv) * 1024);
-    const int stages[3] = {nenv ? std::max(1, std::min(3, atoi(nenv))) : 2, 2, 1};
+    int stages[3] = {nenv ? std::max(1, std::min(3, atoi(nenv))) : 2, 2, 1};
+    if (T > 128 && !benv && !nenv) {
+        // b-tiles are single frames here (FT_max = 1) and items are a-frame chunks whose
+        // fixed part (b-row entries, row tables) is amortised over the chunk: one 220 KB
+        // stage per SM (wider chunks, half the items) measured faster than two 110 KB
+        // stages or two 220 KB ones (single instance, T = 320: 7.3 -> 4.7 ms)
+        budgets[0] = std::min(budgets[2], (size_t)220 * 1024);
+        stages[0] = 1;
+    }
     // stage bytes of the unclipped item: b-frames [a, b), a-frames [g0, g1)
     auto foot = [&](int64_t a, int64_t b, int64_t g0, int64_t g1, int64_t book) {
         return (int64_t)item_stage_bytes((int)(QP(b) - QP(a)), (int)(QP(g1) - QP(g0)), (int)(NF(b + T - 1) - NF(a)),
