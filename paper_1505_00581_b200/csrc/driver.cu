@@ -324,20 +324,6 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
     }
     const char *cenv = getenv("HGM_CHUNK");  // windows per chunk (tuning knob)
     const int chunk_max = std::min(65535, cenv && atoi(cenv) > 0 ? atoi(cenv) : 4096);
-    const char *senv = getenv("HGM_STREAMS");  // 2: alternate chunks over two streams (measured slower)
-    const int nlanes = (senv && atoi(senv) == 2) ? 2 : 1;
-    struct Lane {
-        cudaStream_t s = nullptr;
-        DevBuf hist, items, counters, book;
-        int64_t hist_cap = 0, items_cap = 0, counters_cap = 0, book_cap = 0;
-    } lanes[2];
-    lanes[0].s = s;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    if (nlanes == 2) {
-        lanes[1].s = aux_stream(sc->device);
-        HGM_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-        HGM_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
-    }
     // Chunks of windows (the alpha history of a chunk fits the budget), every window's
     // layer offset and work-item count, planned up front so that the window
     // descriptors and item prefixes reach the device in one copy each (no per-chunk
@@ -366,6 +352,26 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
         max_items = std::max<int64_t>(max_items, c.nitems);
         chunks.push_back(c);
         k0 = c.k1;
+    }
+    // Two lanes (chunks alternate over two streams, each with its own buffers) when the
+    // chunks are few-window ones (long chains / wide windows: C4): a chunk's last DP
+    // steps and its backtrack leave the GPU mostly idle, the other lane fills it
+    // (C4, ~8 windows per chunk: 21-32 % less time per call).  Many-window chunks (C3,
+    // ~800 per 6 GiB chunk) are faster on one lane, and a second lane doubles the history.
+    const char *senv = getenv("HGM_STREAMS");  // 1 / 2: force
+    const int nlanes = senv ? (atoi(senv) == 2 ? 2 : 1)
+                            : ((chunks.size() >= 3 && (int64_t)count < 64 * (int64_t)chunks.size()) ? 2 : 1);
+    struct Lane {
+        cudaStream_t s = nullptr;
+        DevBuf hist, items, counters, book;
+        int64_t hist_cap = 0, items_cap = 0, counters_cap = 0, book_cap = 0;
+    } lanes[2];
+    lanes[0].s = s;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    if (nlanes == 2) {
+        lanes[1].s = aux_stream(sc->device);
+        HGM_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+        HGM_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     }
     DevBuf d_all, d_ibase;
     HGM_TRY(d_all.alloc(sizeof(InstDesc) * count, s));

@@ -4,7 +4,9 @@ fraction of the 10.5-issue-slot roofline for C1, C2, C4 (T in {10,20,40,80}; rho
 754-node scene: W = stride = 60 and W = 723).  Inputs HBM-resident (scene index and
 model graphs built untimed), CUDA events around `steps` detect_actions calls after
 `warmup`; SM clock sampled through NVML right after the timed region.  C3 is
-bench.py's headline.  One JSON line per row."""
+bench.py's headline.  One JSON line per row.  `frac` uses the K-DP event time; with two
+lanes (C4) those intervals overlap the other lane's work, so read `frac_wall` there
+(candidates / whole call time / roofline: a lower bound on the kernel's fraction)."""
 import argparse
 import json
 import sys
@@ -91,6 +93,7 @@ for name, models_pts, scenes_pts, stride, count, W, p in rows():
     print(json.dumps(dict(config=name, pairs=pairs, ms_per_call=round(ms, 4), pairs_per_s=round(pairs / ms * 1e3, 1),
                           dp_ms=round(dp_ms, 4), dp_share=round(dp_ms / ms, 3), real_candidates=int(cand),
                           dp_gcand_s=round(ach, 1), roofline_gcand_s=round(roof, 1), frac=round(ach / roof, 4),
+                          frac_wall=round(cand / (ms / 1e3) / 1e9 / roof, 4),
                           sm_mhz=f, kernel_ms={k: round(v / a.steps, 4) for k, v in st["ms"].items() if v},
                           l2="no flush between calls (configs re-read their inputs; C2/C4 exceed L2 only partly)")),
           flush=True)
