@@ -144,29 +144,55 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------- oracle
-def oracle_sample_rate(wl, target_s, seed=0, max_pairs=4096):
-    """Time the CPU oracle (as it stands) on a bounded random sample of pairs."""
-    import oracle
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
-    ncores = os.cpu_count() or 1
+
+def oracle_sample_rate(wl, target_s, seed=0, max_pairs=4096, threads=None):
+    """Time the CPU oracle (as it stands) on a bounded random sample of pairs, on
+    `threads` host threads (default: every core).  Also counts the sample's real-triple
+    candidates (work.py, exact) for a candidates/s figure."""
+    import oracle
+    from paper_1505_00581_b200.work import count_work
+
+    ncores = threads or os.cpu_count() or 1
     models = [oracle.model_nodes(m) for m in wl["models"]]
     order, scene = oracle.scene_nodes(wl["scene"])
     rng = np.random.default_rng(seed)
+    per_off = count_work(wl["scene"].frame, wl["first"], wl["stride"], wl["count"], wl["window"],
+                         wl["params"]["T"], per_offset=True)
 
     def run(n):
         ks = rng.integers(0, wl["count"], n)
         ms = rng.integers(0, len(models), n)
         wins = [oracle.window_range(scene.t, wl["first"] + int(k) * wl["stride"], wl["window"]) for k in ks]
         t0 = time.perf_counter()
-        E, _, _, _ = oracle.match_batch(models, scene, wl["params"], ms, [w[0] for w in wins], [w[1] for w in wins],
+        E, _, A, z = oracle.match_batch(models, scene, wl["params"], ms, [w[0] for w in wins], [w[1] for w in wins],
                                         ncores)
-        return time.perf_counter() - t0, list(zip(ms.tolist(), ks.tolist())), E
+        dt = time.perf_counter() - t0
+        cand = sum(int(per_off[k]) * max(models[m].n - 2, 0) for m, k in zip(ms.tolist(), ks.tolist()))
+        return dt, list(zip(ms.tolist(), ks.tolist())), E, A, z, cand
 
-    dt, _, _ = run(ncores)
+    dt, _, _, _, _, _ = run(ncores)
     rate = ncores / max(dt, 1e-6)
     n = int(min(max(ncores, rate * target_s), max_pairs))
-    dt, pairs, E = run(n)
-    return dict(value=n / dt, unit="pairs/s", cores=ncores, kind="oracle", elapsed_s=dt, pairs=pairs, E=E,
+    dt, pairs, E, A, z, cand = run(n)
+    return dict(value=n / dt, unit="pairs/s", cores=ncores, kind="oracle", elapsed_s=dt, pairs=pairs, E=E, A=A, z=z,
+                candidates_per_s=cand / dt,
                 sample=f"{n} uniformly drawn (model, offset) pairs of rank 0's workload, seed {seed}, "
                        f"fp64 C oracle, {ncores} threads")
 
@@ -194,8 +220,29 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------------- own arm
+def spawn_ranks(args):
+    """`--gpus N` without a launcher: re-exec this command under torch.distributed.run
+    (one process per GPU, rendezvous on 127.0.0.1) and return its exit code."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # NCCL's init log (transport, NVLS) stays visible on stderr
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    print(f"bench.py: spawning {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args))
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']} (launcher mismatch)")
     if args.impl == "reference":
         return run_reference(args)
     import torch
@@ -313,9 +360,13 @@ def main():
     # roofline of the dominant kernel (K-DP), ALU-bound
     dp_ms = st["ms"]["dp"] / args.steps
     f_mhz = ck["sm_mhz"] or 1965.0
-    achieved = work_cand / (dp_ms / 1000.0) / 1e9  # G real-triple candidates / s
+    # % of roofline = (10.5 N_rrr + 2 N_states) / (t x 18,944 x f_SM); expressed in
+    # candidate-equivalents (the per-state FADD + min counted as 2/10.5 of a candidate)
+    cand_eq = work_cand + 2.0 * work_states / ISSUE_SLOTS_PER_CAND
+    achieved = cand_eq / (dp_ms / 1000.0) / 1e9  # G candidate-equivalents / s
     peak = LANES_PER_CLK * f_mhz * 1e6 / ISSUE_SLOTS_PER_CAND / 1e9
     xu_peak = XU_LANES_PER_CLK * f_mhz * 1e6 / 1e9  # G model-candidates / s (one MUFU.SQRT each)
+    cand_rate = work_cand / (dp_ms / 1000.0) / 1e9
     traffic, traffic_src = None, None
     tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "dp_traffic.json")
     if os.path.exists(tpath):  # DRAM bytes per K-DP launch from the committed ncu --set full capture
@@ -323,8 +374,10 @@ def main():
             tj = json.load(fh)
         traffic, traffic_src = tj.get("dram_bytes_per_launch"), tj.get("source")
     roof = dict(bound="alu", achieved=achieved, peak=peak, unit="Gcand/s", frac=achieved / peak, traffic=traffic,
+                achieved_basis="(real-triple candidates + 2/10.5 x states) / K-DP device time (SURVEY §8(d) formula)",
+                candidates_per_s_g=cand_rate, frac_candidates_only=cand_rate / peak,
                 traffic_unit="DRAM bytes per K-DP launch", traffic_source=traffic_src,
-                xu_peak=xu_peak, xu_frac=achieved / xu_peak,
+                xu_peak=xu_peak, xu_frac=cand_rate / xu_peak,
                 xu_basis="one MUFU.SQRT per model-candidate; 148 SMs x 15.9 lanes/clk (measured) x SM clock",
                 kernel="k_dp_fused", dp_ms_per_step=dp_ms, dp_share_of_step=dp_ms / ms_step,
                 candidates_per_step=work_cand, states_per_step=work_states,
@@ -398,14 +451,44 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         r = oracle_sample_rate(wl, args.cpu_seconds)
-        # parity spot-check of the timed configuration on the sampled pairs
+        # parity spot-check of the timed configuration on the sampled pairs: detect's E of
+        # every sampled pair, and each model's assignments (match_model_at_offsets) against
+        # the oracle's z, a differing z accepted only under the near-tie rule
+        from tests._parity import Checker
+
         models = [hgm.build_model_graph(m) for m in models_d]
         scene = hgm.build_scene_index(scene_d, T_max=p["T"])
         det = hgm.detect_actions(models, scene, p, first, stride, count, W, want_E_all=True)
         Eg = det.E_all.cpu().numpy()
         errs = [abs(float(Eg[m, k]) - e) / (1e-6 + 1e-5 * abs(e)) for (m, k), e in zip(r["pairs"], r["E"])]
+        chk = Checker(wl["models"], wl["scene"], p, first, stride, W)
+        ids = wl["scene"].ids()[chk.order]
+        per_model = {}
+        z_bad, z_ties, z_eq = [], 0, 0
+        for j, (m, k) in enumerate(r["pairs"]):
+            if m not in per_model:
+                rm = hgm.match_model_at_offsets(models[m], scene, p, first, stride, count, W, device_out=False)
+                per_model[m] = rm
+            rm = per_model[m]
+            zo = np.where(r["z"][j] >= 0, ids[np.maximum(r["z"][j], 0)], -1)
+            msg = chk.check_pair(m, k, rm.E[k], rm.A[k], rm.z[k], r["E"][j], r["A"][j], zo)
+            if msg is None:
+                z_eq += 1
+            elif msg == "TIE":
+                z_ties += 1
+            else:
+                z_bad.append(msg)
+        r1 = oracle_sample_rate(wl, max(3.0, args.cpu_seconds / 4), seed=1, threads=1)
         cpu = dict(value=r["value"], unit="pairs/s", cores=r["cores"], kind="oracle", sample=r["sample"],
-                   parity_max_err_over_tol=max(errs) if errs else None)
+                   cpu_model=cpu_model(), candidates_per_s=r["candidates_per_s"],
+                   frames_per_s_extrapolated=r["value"] / n_models * stride,
+                   frames_per_s_note="extrapolated: pairs/s / models x stride (every offset matches every model)",
+                   single_thread=dict(value=r1["value"], unit="pairs/s", candidates_per_s=r1["candidates_per_s"],
+                                      frames_per_s_extrapolated=r1["value"] / n_models * stride,
+                                      sample=r1["sample"]),
+                   parity_max_err_over_tol=max(errs) if errs else None,
+                   parity_z=dict(pairs=len(r["pairs"]), identical=z_eq, near_ties=z_ties, failures=len(z_bad),
+                                 first_failure=z_bad[0] if z_bad else None))
 
     if rank == 0:
         line = dict(metric=BASELINE_METRIC, value=value, unit="pairs/s", n_gpus=world, steps=args.steps,

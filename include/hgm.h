@@ -34,7 +34,9 @@ typedef enum {
     HGM_ERR_DIMENSION_MISMATCH = 2,  /* descriptor length F differs between model(s) and scene */
     HGM_ERR_INVALID_ARGUMENT = 3,    /* NULL pointer, non-finite or negative lambda / W^d,
                                         T < 1, T > scene T_max, window < 1, stride < 1,
-                                        count < 0, negative frame, size overflow */
+                                        count < 0, negative frame, frame > 2^26, offsets
+                                        beyond +-2^26 frames, non-finite x / y / saliency /
+                                        descriptor component, size overflow */
     HGM_ERR_OUT_OF_MEMORY = 4,       /* device allocation failed */
     HGM_ERR_CUDA = 5                 /* any other CUDA runtime error (incl. no device) */
 } hgm_status;
@@ -47,7 +49,7 @@ typedef struct hgm_scene hgm_scene; /* opaque: sorted scene + frame index + dire
 typedef struct {
     int64_t n;              /* number of points */
     int32_t F;              /* descriptor length (162 for HoG/HoF) */
-    const int32_t *frame;   /* [n] integer frame t >= 0 */
+    const int32_t *frame;   /* [n] integer frame, 0 <= t <= 2^26 (a video's frame numbers) */
     const float *x, *y;     /* [n] pixel position */
     const float *saliency;  /* [n] detector confidence; used by the model builder only */
     const float *feat;      /* [n*F] row-major descriptors f */
@@ -74,7 +76,9 @@ typedef struct {
  *   host variant: `pts` arrays are host memory; synchronous.
  *   dev  variant: `pts` arrays are device memory on `device`'s context;
  *                 runs on `stream`, returns after the handle is ready.
- * Errors: n == 0 -> EMPTY_POINT_SET; NULL arrays / F < 1 -> INVALID_ARGUMENT. */
+ * Errors: n == 0 -> EMPTY_POINT_SET; NULL arrays / F < 1 / a non-finite coordinate,
+ * saliency or descriptor component / a frame outside [0, 2^26] -> INVALID_ARGUMENT
+ * (saliency may be NULL: all points equally salient). */
 hgm_status hgm_build_model_graph(const hgm_points *pts, int device, hgm_model **out);
 hgm_status hgm_build_model_graph_dev(const hgm_points *pts, void *stream, hgm_model **out);
 /* Independent chains ("Multiple points 2: creation of
@@ -93,8 +97,13 @@ void hgm_free_model(hgm_model *model);
  * frame; minnode(f) = first node with frame >= f (sentinel S, R4); and the
  * band of ordered node pairs (a, c) with 1 <= t'(c) - t'(a) <= T_max - 1
  * holding the direction of a->c and a coincidence flag.
- * T_max bounds the T of later calls.  Same host / dev split as above.
- * Errors: n == 0 -> EMPTY_POINT_SET; T_max < 1 -> INVALID_ARGUMENT. */
+ * T_max bounds the T of later calls.  Any T_max (and any later T) above the scene's
+ * frame span is legal and means "unpruned": the band is built for
+ * min(T_max, last frame + 1), which admits every pair, and calls run with
+ * min(T, last frame + 1) -- the same result, no integer overflow.
+ * Same host / dev split as above.
+ * Errors: n == 0 -> EMPTY_POINT_SET; T_max < 1, a frame outside [0, 2^26], a non-finite
+ * coordinate or descriptor component -> INVALID_ARGUMENT. */
 hgm_status hgm_build_scene_index(const hgm_points *pts, int device, int32_t T_max, hgm_scene **out);
 hgm_status hgm_build_scene_index_dev(const hgm_points *pts, int32_t T_max, void *stream, hgm_scene **out);
 hgm_status hgm_scene_num_nodes(const hgm_scene *scene, int64_t *S);
@@ -148,7 +157,9 @@ hgm_status hgm_detect_chains(const hgm_model *const *chains, int32_t n_chains, c
  *   (o + W <= seen), writing *n_out results (winner / score as hgm_detect_actions, host
  *   or device, capacity entries available) for offsets *first_offset + j * stride.
  *   Results are identical to one hgm_detect_actions call over the whole stream.
- *   Synchronous.  Errors: NULL st / n_out / first_offset, n_frames < 0, points outside
+ *   Synchronous.  A push that fails (any status) leaves the stream unchanged: its frames
+ *   are not consumed and the same push may be retried.
+ *   Errors: NULL st / n_out / first_offset, n_frames < 0, points outside
  *   the pushed frames, capacity too small -> INVALID_ARGUMENT; F differing from the
  *   models' -> DIMENSION_MISMATCH; CUDA errors as elsewhere.  Windows without points
  *   (silent stretches) are valid and give the all-dummy result. */

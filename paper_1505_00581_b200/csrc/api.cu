@@ -1,7 +1,10 @@
 // api.cu -- the extern "C" surface of libhgm.so (include/hgm.h): argument
 // checks, handle ownership, host/device buffer staging, kernel timing.
 // All computation happens in the kernels of scene.cu, unary.cu and dp.cu.
+#include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -164,7 +167,19 @@ static hgm_status check_offsets(const hgm_offsets *o) {
     if (!o) return fail(HGM_ERR_INVALID_ARGUMENT, "offsets == NULL");
     if (o->window < 1 || o->stride < 1 || o->count < 0)
         return fail(HGM_ERR_INVALID_ARGUMENT, "window < 1, stride < 1 or count < 0");
+    // every window frame (and frame + T inside the kernels) must stay far inside int32
+    const int64_t last = (int64_t)o->first_frame + (int64_t)(o->count > 0 ? o->count - 1 : 0) * o->stride + o->window;
+    if ((int64_t)o->first_frame < -(int64_t)HGM_MAX_FRAME || last > 2 * (int64_t)HGM_MAX_FRAME)
+        return fail(HGM_ERR_INVALID_ARGUMENT, "offsets reach beyond +-2^26 frames");
     return HGM_OK;
+}
+
+// T at or above the scene's frame span + 1 admits every pair (t'(c) - t'(a) <= fmax < T):
+// the kernels run with min(T, fmax + 1), the same result without int overflow in t + T
+static hgm_params effective_params(const hgm_params *p, const hgm_scene *sc) {
+    hgm_params e = *p;
+    e.T = (int32_t)std::min<int64_t>(e.T, (int64_t)sc->fmax + 1);
+    return e;
 }
 
 // Copy a host point set to the device (borrowed input, copied per the ABI).
@@ -375,14 +390,17 @@ hgm_status hgm_match_model_at_offsets(const hgm_model *model, const hgm_scene *s
     covered_range(scene, offsets, &n_lo, &n_hi);
     const int64_t nn = std::max<int64_t>(n_hi - n_lo, 1);
     DevBuf U, dE, dA, dz;
-    HGM_TRY(U.alloc(sizeof(float) * ((size_t)model->M * nn + 4), s));  // + 16 B: K-DP bulk-copy rounding
-    HGM_TRY(unary_table(model->feat, model->M, 1, model->Fp, scene, n_lo, n_hi, U.as<float>(), s));
+    const int64_t ustr = unary_stride(model->M, 1, nn);  // raw U, then lambda1 U
+    HGM_TRY(U.alloc(sizeof(float) * 2 * (size_t)ustr, s));
+    HGM_TRY(unary_table(model->feat, model->M, 1, model->Fp, scene, n_lo, n_hi, params->lambda1, U.as<float>(),
+                        U.as<float>() + ustr, s));
     const bool hE = E && !is_device_ptr(E), hA = A && !is_device_ptr(A), hz = z && !is_device_ptr(z);
     if (hE) HGM_TRY(dE.alloc(sizeof(float) * count, s));
     if (hA) HGM_TRY(dA.alloc(sizeof(float) * count, s));
     if (hz) HGM_TRY(dz.alloc(sizeof(int64_t) * (size_t)count * model->M, s));
     MatchOut mo{hE ? dE.as<float>() : E, hA ? dA.as<float>() : A, hz ? dz.as<int64_t>() : z};
-    HGM_TRY(match_batch(&model, 1, scene, *params, *offsets, U.as<float>(), n_lo, nn, &mo, s));
+    const hgm_params pe = effective_params(params, scene);
+    HGM_TRY(match_batch(&model, 1, scene, pe, *offsets, U.as<float>(), U.as<float>() + ustr, n_lo, nn, &mo, s));
     scene->uses.record(s);
     model->uses.record(s);
     if (hE) HGM_CUDA(cudaMemcpyAsync(E, dE.p, sizeof(float) * count, cudaMemcpyDeviceToHost, s));
@@ -417,15 +435,20 @@ static hgm_status detect_scores(const hgm_model *const *models, int32_t n_models
         for (int k = 0; k < NM; ++k)
             HGM_CUDA(cudaMemcpyAsync(mfeat.as<float>() + (size_t)k * M * Fp, models[m0 + k]->feat,
                                      sizeof(float) * (size_t)M * Fp, cudaMemcpyDeviceToDevice, s));
-        HGM_TRY(U.alloc(sizeof(float) * ((size_t)NM * M * nn + 4), s));  // + 16 B: K-DP bulk-copy rounding
-        HGM_TRY(unary_table(mfeat.as<float>(), M, NM, Fp, scene, n_lo, n_hi, U.as<float>(), s));
+        const int64_t ustr = unary_stride(M, NM, nn);  // raw U, then lambda1 U
+        HGM_TRY(U.alloc(sizeof(float) * 2 * (size_t)ustr, s));
+        HGM_TRY(unary_table(mfeat.as<float>(), M, NM, Fp, scene, n_lo, n_hi, params->lambda1, U.as<float>(),
+                            U.as<float>() + ustr, s));
         MatchOut mo[MAX_BATCH_API];
         for (int k = 0; k < NM; ++k)
             mo[k] = MatchOut{Ed + (size_t)(m0 + k) * count, Ad + (size_t)(m0 + k) * count,
                              zb.as<int64_t>() + (size_t)k * count * Mmax};
         g_tiling_failed = false;
-        const hgm_status bst = match_batch(models + m0, NM, scene, *params, *offsets, U.as<float>(), n_lo, nn, mo, s);
+        const hgm_params pe = effective_params(params, scene);
+        const hgm_status bst =
+            match_batch(models + m0, NM, scene, pe, *offsets, U.as<float>(), U.as<float>() + ustr, n_lo, nn, mo, s);
         if (bst != HGM_OK && g_tiling_failed && NM > 1) {
+            if (getenv("HGM_DEBUG_TILING")) fprintf(stderr, "tiling: batch of %d retried one model at a time\n", NM);
             max_batch = 1;  // too dense for a batch's stage: one model at a time from here on
             m1 = m0;
             continue;

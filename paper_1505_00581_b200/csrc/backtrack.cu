@@ -43,6 +43,7 @@ __device__ __forceinline__ void init_search(const SceneView &sc, const InstDesc 
     const int Sw = d.we - d.wb, M = bt.M, T = p.T, SS = bt.SS;
     const int EPSL = d.we;
     auto Uk = [&](int i, int n, int k) { return __ldg(bt.U + ((int64_t)i * bt.nn + (n - bt.n_lo)) * NM + k); };
+    auto Usk = [&](int i, int n, int k) { return __ldg(bt.Us + ((int64_t)i * bt.nn + (n - bt.n_lo)) * NM + k); };
     Best best[NM];
 #pragma unroll
     for (int k = 0; k < NM; ++k) best[k] = Best{INFINITY, 0x7fffffff, 0x7fffffff};
@@ -50,7 +51,7 @@ __device__ __forceinline__ void init_search(const SceneView &sc, const InstDesc 
         for (int c = d.wb + q0 + tid; c <= d.we; c += qs) {
 #pragma unroll
             for (int k = 0; k < NM; ++k) {
-                const Best x{c < d.we ? __fmul_rn(p.l1, Uk(0, c, k)) : p.l1W, c, 0};
+                const Best x{c < d.we ? Usk(0, c, k) : p.l1W, c, 0};
                 if (better(x, best[k])) best[k] = x;
             }
         }
@@ -81,8 +82,8 @@ __device__ __forceinline__ void init_search(const SceneView &sc, const InstDesc 
             if (!ok) continue;
 #pragma unroll
             for (int k = 0; k < NM; ++k) {
-                const float u1 = z1 < EPSL ? __fmul_rn(p.l1, Uk(0, z1, k)) : p.l1W;
-                const float u2 = z2 < EPSL ? __fmul_rn(p.l1, Uk(1, z2, k)) : p.l1W;
+                const float u1 = z1 < EPSL ? Usk(0, z1, k) : p.l1W;
+                const float u2 = z2 < EPSL ? Usk(1, z2, k) : p.l1W;
                 const float a = M > 2 ? __ldg(a3 + (int64_t)slot * SS + k) : 0.f;
                 const Best x{__fadd_rn(__fadd_rn(u1, u2), a), z1, z2};
                 if (better(x, best[k])) best[k] = x;
@@ -133,6 +134,7 @@ __global__ void __launch_bounds__(256) k_backtrack(SceneView sc, const InstDesc 
     const int Sw = d.we - d.wb, M = bt.M, T = p.T, SS = bt.SS;
     const int EPSL = d.we;  // dummy label: orders after every real node (R11)
     auto Uk = [&](int i, int n, int k) { return __ldg(bt.U + ((int64_t)i * bt.nn + (n - bt.n_lo)) * NM + k); };
+    auto Usk = [&](int i, int n, int k) { return __ldg(bt.Us + ((int64_t)i * bt.nn + (n - bt.n_lo)) * NM + k); };
     auto layer = [&](int i) -> const float * {
         return (i >= 2 && i <= M - 1) ? hist + (int64_t)(i - 2) * L + d.off : nullptr;
     };
@@ -155,7 +157,8 @@ __global__ void __launch_bounds__(256) k_backtrack(SceneView sc, const InstDesc 
             if (better(y, bst)) bst = y;
         }
     }
-    auto U = [&](int i, int n) { return Uk(i, n, kk); };
+    auto U = [&](int i, int n) { return Uk(i, n, kk); };     // raw (A)
+    auto Us = [&](int i, int n) { return Usk(i, n, kk); };   // lambda1 U (the recursion)
     auto at = [&](const float *l, int s) { return atk(l, s, kk); };
     auto a_be = [&](const float *l, int b) { return at(l, d.ntail + (b - d.wb)); };
     auto a_ea = [&](const float *l, int a) { return at(l, d.ntail + Sw + (a - d.wb)); };
@@ -202,14 +205,14 @@ __global__ void __launch_bounds__(256) k_backtrack(SceneView sc, const InstDesc 
         auto value = [&](int c) -> float {
             const int j = c - c0;
             if (rb) {
-                const float n = msg_n(at(nx, qbp + j), p.l1, U(i, c));
+                const float n = msg_n(at(nx, qbp + j), Us(i, c));
                 if (!ra) return n;
                 const float m = msg_m(n, p.l2, kc.x, sc.t[c] - tb);
                 const bool cbc = sc.coinc[qb + j];
                 return cand_value(m, sc.theta[qb + j], th_ab, sc.theta[qa + aoff + j], cbc || co_ab,
                                   cbc || sc.coinc[qa + aoff + j], kc.z, kc.w, p.l23);
             }
-            return msg_n(a_be(nx, c), p.l1, U(i, c));
+            return msg_n(a_be(nx, c), Us(i, c));
         };
         // minimum and first argmin (ascending c): groups of 4 x 32 candidates, a lane's
         // 4 evaluations independent (their loads overlap); per group the lane keeps its

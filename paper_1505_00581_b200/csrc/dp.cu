@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(256) k_dp_step(SceneView sc, const InstDesc *_
         int p_ac = sc.qstart[a] + (c0 - lo_a); // pair (a -> c)
         float R = INFINITY;
         for (int c = c0; c < c1; ++c, ++p_bc, ++p_ac) {
-            const float ncb = msg_n(nxt ? nxt[p_bc - d.pbase] : 0.f, p.l1, Ui[c]);
+            const float ncb = msg_n(nxt ? nxt[p_bc - d.pbase] : 0.f, Ui[c]);
             const float m = msg_m(ncb, p.l2, k.g_i, sc.t[c] - tb);
             const bool cbc = sc.coinc[p_bc];
             R = fminf(R, cand_value(m, sc.theta[p_bc], th_ab, sc.theta[p_ac], cbc || co_ab, cbc || sc.coinc[p_ac],
@@ -71,18 +71,18 @@ __global__ void __launch_bounds__(256) k_dp_step(SceneView sc, const InstDesc *_
         const int c0 = sc.first(tb + 1), c1 = min(sc.first(tb + p.T), d.we);
         int p_bc = sc.qstart[b];
         float R = INFINITY;
-        for (int c = c0; c < c1; ++c, ++p_bc) R = fminf(R, msg_n(nxt ? nxt[p_bc - d.pbase] : 0.f, p.l1, Ui[c]));
+        for (int c = c0; c < c1; ++c, ++p_bc) R = fminf(R, msg_n(nxt ? nxt[p_bc - d.pbase] : 0.f, Ui[c]));
         out = fminf(R, __fadd_rn(p.l1W, nxt ? nxt[d.np + Sw + (b - d.wb)] : 0.f));
     } else if (s < d.np + 2 * Sw) {  // (eps, a): c constrained by a alone (R5)
         const int a = d.wb + (s - d.np - Sw);
         const int ta = sc.t[a];
         const int c0 = sc.first(ta + 1), c1 = min(sc.first(ta + p.T), d.we);
         float R = INFINITY;
-        for (int c = c0; c < c1; ++c) R = fminf(R, msg_n(nxt ? nxt[d.np + (c - d.wb)] : 0.f, p.l1, Ui[c]));
+        for (int c = c0; c < c1; ++c) R = fminf(R, msg_n(nxt ? nxt[d.np + (c - d.wb)] : 0.f, Ui[c]));
         out = fminf(R, __fadd_rn(p.l1W, nxt ? nxt[d.np + 2 * Sw] : 0.f));
     } else {  // (eps, eps): unconstrained within the window
         float R = INFINITY;
-        for (int c = d.wb; c < d.we; ++c) R = fminf(R, msg_n(nxt ? nxt[d.np + (c - d.wb)] : 0.f, p.l1, Ui[c]));
+        for (int c = d.wb; c < d.we; ++c) R = fminf(R, msg_n(nxt ? nxt[d.np + (c - d.wb)] : 0.f, Ui[c]));
         out = fminf(R, __fadd_rn(p.l1W, nxt ? nxt[d.np + 2 * Sw] : 0.f));
     }
     cur[s] = out;
@@ -97,7 +97,8 @@ __global__ void k_backtrack(SceneView sc, const InstDesc *__restrict__ inst, int
     if (k >= ninst) return;
     const InstDesc d = inst[k];
     const int Sw = d.we - d.wb, EPS = -1, M = bt.M;
-    auto U = [&](int i, int n) { return bt.U[(int64_t)i * bt.nn + (n - bt.n_lo)]; };
+    auto U = [&](int i, int n) { return bt.U[(int64_t)i * bt.nn + (n - bt.n_lo)]; };     // raw (A)
+    auto Us = [&](int i, int n) { return bt.Us[(int64_t)i * bt.nn + (n - bt.n_lo)]; };   // lambda1 U
     auto layer = [&](int i) -> const float * {  // alpha_i for 0-based step i (2..M-1); null = alpha == 0
         return (i >= 2 && i <= M - 1) ? hist + (int64_t)(i - 2) * L + d.off : nullptr;
     };
@@ -115,14 +116,14 @@ __global__ void k_backtrack(SceneView sc, const InstDesc *__restrict__ inst, int
     float best = INFINITY;
     if (M == 1) {
         for (int c = d.wb; c <= d.we; ++c) {
-            const float v = c < d.we ? __fmul_rn(p.l1, U(0, c)) : p.l1W;
+            const float v = c < d.we ? Us(0, c) : p.l1W;
             if (v < best) { best = v; z1b = c < d.we ? c : EPS; }
         }
     } else {
         const float *a3 = layer(2);
         for (int z1 = d.wb; z1 <= d.we; ++z1) {
             const bool r1 = z1 < d.we;
-            const float u1 = r1 ? __fmul_rn(p.l1, U(0, z1)) : p.l1W;
+            const float u1 = r1 ? Us(0, z1) : p.l1W;
             int c0 = d.wb, c1 = d.we;
             if (r1) {
                 c0 = sc.first(sc.t[z1] + 1);
@@ -130,7 +131,7 @@ __global__ void k_backtrack(SceneView sc, const InstDesc *__restrict__ inst, int
             }
             for (int z2 = c0; z2 <= c1; ++z2) {
                 const bool r2 = z2 < c1;
-                const float u2 = r2 ? __fmul_rn(p.l1, U(1, z2)) : p.l1W;
+                const float u2 = r2 ? Us(1, z2) : p.l1W;
                 float al;
                 if (r1 && r2) al = a_pair(a3, z2, z1);
                 else if (r1) al = a_ea(a3, z1);
@@ -165,7 +166,7 @@ __global__ void k_backtrack(SceneView sc, const InstDesc *__restrict__ inst, int
             int arg = EPS;
             int p_bc = sc.qstart[zb], p_ac = sc.qstart[za] + (c0 - lo_a);
             for (int c = c0; c < c1; ++c, ++p_bc, ++p_ac) {
-                const float ncb = msg_n(nx ? nx[p_bc - d.pbase] : 0.f, p.l1, U(i, c));
+                const float ncb = msg_n(nx ? nx[p_bc - d.pbase] : 0.f, Us(i, c));
                 const float m = msg_m(ncb, p.l2, kc.x, sc.t[c] - tb);
                 const bool cbc = sc.coinc[p_bc];
                 const float v = cand_value(m, sc.theta[p_bc], th_ab, sc.theta[p_ac], cbc || co_ab,
@@ -180,7 +181,7 @@ __global__ void k_backtrack(SceneView sc, const InstDesc *__restrict__ inst, int
             const int c0 = sc.first(tb + 1), c1 = min(sc.first(tb + p.T), d.we);
             int arg = EPS, p_bc = sc.qstart[zb];
             for (int c = c0; c < c1; ++c, ++p_bc) {
-                const float v = msg_n(nx ? nx[p_bc - d.pbase] : 0.f, p.l1, U(i, c));
+                const float v = msg_n(nx ? nx[p_bc - d.pbase] : 0.f, Us(i, c));
                 if (v < R) { R = v; arg = c; }
             }
             zc = (R <= __fadd_rn(p.l1W, a_ea(nx, zb)) && arg != EPS) ? arg : EPS;
@@ -192,7 +193,7 @@ __global__ void k_backtrack(SceneView sc, const InstDesc *__restrict__ inst, int
             }
             int arg = EPS;
             for (int c = c0; c < c1; ++c) {
-                const float v = msg_n(a_be(nx, c), p.l1, U(i, c));
+                const float v = msg_n(a_be(nx, c), Us(i, c));
                 if (v < R) { R = v; arg = c; }
             }
             zc = (R <= __fadd_rn(p.l1W, a_ee(nx)) && arg != EPS) ? arg : EPS;

@@ -40,8 +40,9 @@
 // backtrack's re-evaluation (backtrack.cu) stays bit-identical.
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
-#include "dp_common.cuh"
+#include "dp_kdp.cuh"
 
 namespace hgm {
 
@@ -61,7 +62,6 @@ constexpr int KDP_WARPS = KDP_THREADS / 32;
 constexpr int KDP_BLOCK = KDP_THREADS + 32;      // + one copy warp (claims items, issues their TMA copies)
 constexpr int NROWI = 6;  // derived row bookkeeping ints per row
 
-__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
 // Per-item bookkeeping that does not change from step to step (computed once per
 // chunk by k_item_prep, copied into the stage with the item's other inputs):
@@ -107,7 +107,7 @@ struct StageLayout {
         uc = take(4LL * (NM * NC + 8));
         we = take(4LL * (EPF * NC + 8));
         tc = take(4LL * (NC + 8));
-        ni = take(16LL * (NA + 1));
+        ni = take(16LL * (NB + 1));  // node info of the b rows
         eb = take(4LL * (EPF * NB + 8));
         ee = take(4LL * (EPF + 8));
         ftab = take(4LL * (FT + 2 * T + 16));
@@ -118,7 +118,8 @@ struct StageLayout {
 };
 
 __host__ __device__ inline StageLayout item_layout(const WorkItem &w, int T, int NM, int book) {
-    return StageLayout(w.qb1 - w.qb0, w.qa1 - w.qa, w.Cend - w.B0, w.B1 - w.A0, w.B1 - w.B0, w.F1 - w.F0, T, NM, book);
+    return StageLayout(w.qb1 - w.qb0, w.qa1 - w.qa, w.Cend - w.B0, w.nA + (w.B1 - w.B0), w.B1 - w.B0, w.F1 - w.F0, T,
+                       NM, book);
 }
 
 // Shared memory: two stages of caps.STAGE bytes (the largest item layout of the call;
@@ -143,125 +144,6 @@ struct SmemPlan {
     }
 };
 
-// ------------------------------------------------------------------ TMA bulk copies
-__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-// try_wait with a short suspend-time hint: the waiting warp sleeps in hardware (no
-// polling instructions) and oversleeps the phase completion by at most ~hint_ns (a
-// 1 ms hint was seen to oversleep by that much).
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity, unsigned hint_ns = 256) {
-    unsigned ok = 0;
-    do {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(ok)
-            : "r"(smem_u32(bar)), "r"(parity), "r"(hint_ns)
-            : "memory");
-    } while (!ok);
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-
-// Bulk copies into one mbarrier's phase: each copy first raises the phase's expected
-// transaction count (mbarrier.expect_tx, no arrival), then one arrival closes the
-// phase's arrival count once every copy is issued.
-struct Copier {
-    uint64_t *bar;
-    unsigned total = 0;
-    __device__ __forceinline__ explicit Copier(uint64_t *b) : bar(b) {}
-    __device__ __forceinline__ void raw(void *d, const void *s, unsigned bytes) {
-        if (bytes == 0) return;
-        asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-        bulk_g2s(d, s, bytes, bar);
-        total += bytes;
-    }
-    // Elements [g0, g1) of a 4-byte-element array, widened to whole 16-byte units
-    // (the allocations carry >= 16 bytes of slack): dst[q] = src[a0 + q], a0 = g0 & ~3.
-    // Returns g0 - a0, the index of element g0 in dst.
-    template <class T>
-    __device__ __forceinline__ int range(void *d, const T *s, int64_t g0, int64_t g1) {
-        static_assert(sizeof(T) == 4, "4-byte elements");
-        const int64_t a0 = g0 & ~(int64_t)3, a1 = (g1 + 3) & ~(int64_t)3;
-        if (g1 > g0) raw(d, s + a0, (unsigned)((a1 - a0) * 4));
-        return (int)(g0 - a0);
-    }
-    __device__ __forceinline__ void close() {
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-    }
-};
-
-__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int u = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += u;
-    }
-    return v;
-}
-
-template <int EPF>
-__device__ __forceinline__ void ld_entry(const float *__restrict__ src, float (&e)[EPF]) {
-#pragma unroll
-    for (int q = 0; q < EPF / 4; ++q) {
-        const float4 v = reinterpret_cast<const float4 *>(src)[q];
-        e[4 * q] = v.x;
-        e[4 * q + 1] = v.y;
-        e[4 * q + 2] = v.z;
-        e[4 * q + 3] = v.w;
-    }
-}
-
-template <int NM>
-__device__ __forceinline__ void st_alpha(float *__restrict__ dst, const float (&v)[NM]) {
-    if constexpr (NM % 2 == 0) {
-#pragma unroll
-        for (int q = 0; q < NM / 2; ++q) reinterpret_cast<float2 *>(dst)[q] = make_float2(v[2 * q], v[2 * q + 1]);
-    } else {
-#pragma unroll
-        for (int q = 0; q < NM; ++q) dst[q] = v[q];
-    }
-}
-
-// v_k = l23 * sqrt((fb - A1_k)^2 + (fc - K2_k)^2) + m_k for every model k; exactly the
-// rounding sequence of cand_value() in hgm_device.cuh, two models per packed op.
-template <int NM>
-__device__ __forceinline__ void cand_values(float fb, float fc, const float *m, const StepConstB &pc, float l23,
-                                            float (&v)[NM]) {
-#pragma unroll
-    for (int q = 0; q < NM / 2; ++q) {
-        const float2 e1 = __fadd2_rn(make_float2(fb, fb), pc.nA1[q]);
-        const float2 e2 = __fadd2_rn(make_float2(fc, fc), pc.nK2[q]);
-        const float2 qq = __ffma2_rn(e1, e1, __fmul2_rn(e2, e2));
-        const float2 s = make_float2(sqrt_approx(qq.x), sqrt_approx(qq.y));
-        const float2 r = __ffma2_rn(make_float2(l23, l23), s, make_float2(m[2 * q], m[2 * q + 1]));
-        v[2 * q] = r.x;
-        v[2 * q + 1] = r.y;
-    }
-    if constexpr (NM % 2 == 1) {
-        constexpr int k = NM - 1;
-        const float e1 = __fadd_rn(fb, pc.nA1[k / 2].x);
-        const float e2 = __fadd_rn(fc, pc.nK2[k / 2].x);
-        v[k] = __fmaf_rn(l23, sqrt_approx(__fmaf_rn(e1, e1, __fmul_rn(e2, e2))), m[k]);
-    }
-}
-
-// mbarrier helpers beyond the TMA ones
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx_noarrive(uint64_t *bar, unsigned bytes) {
-    asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
 
 // Optional pipeline trace (HGM_TRACE=1): globaltimer stamps of CTA 0, one launch.
 __device__ unsigned long long *g_trace = nullptr;
@@ -284,9 +166,6 @@ struct Ctl {
     uint64_t free_[3];  // stage released: one arrival per compute warp
 };
 
-__device__ __forceinline__ void mbar_complete_tx(uint64_t *bar, unsigned n) {
-    asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(n) : "memory");
-}
 
 // Issue the input copies of item (w, d) into stage s (producer lane 0): the alpha_{i+1}
 // rows of the tile's b nodes straight into the candidate-entry area (the layer's state
@@ -317,7 +196,7 @@ __device__ __forceinline__ void issue_stage(const SceneView &sc, WorkItem &w, co
     w.tb0 = cl.range(sb + ly.tb, sc.theta_pad, w.qb0, w.qb1);         // theta(b -> c) of the b rows' entries
     w.uc0 = cl.range(sb + ly.uc, U, ui_off + (int64_t)w.B0 * NM, ui_off + (int64_t)w.Cend * NM);
     w.tc0 = cl.range(sb + ly.tc, sc.t, w.B0, w.Cend);
-    if (w.B1 > w.A0) cl.raw(sb + ly.ni, sc.ninfo + w.A0, (unsigned)(sizeof(int4) * (w.B1 - w.A0)));
+    if (w.B1 > w.B0) cl.raw(sb + ly.ni, sc.ninfo + w.B0, (unsigned)(sizeof(int4) * (w.B1 - w.B0)));
     cl.raw(sb + ly.bk, book + (size_t)w.idx * book_bytes, book_bytes);  // the item's bookkeeping
     const int f_lo = max(0, w.F0 - T), f_hi = min(sc.fmax + 1, w.F1 + T);  // first_tab over [F0 - T, F1 + T]
     w.ft0 = cl.range(sb + ly.ftab, sc.ft, f_lo, f_hi + 1);
@@ -412,14 +291,13 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
                 float wm = INFINITY;
                 const int c1 = first(f + 1);
                 for (int c = first(f); c < c1; ++c)
-                    wm = fminf(wm, msg_n(kHasNext ? WE[w.we0 + (c - B0) * EPF + k] : 0.f, p.l1,
-                                         UC[w.uc0 + (c - B0) * NM + k]));
+                    wm = fminf(wm, msg_n(kHasNext ? WE[w.we0 + (c - B0) * EPF + k] : 0.f, UC[w.uc0 + (c - B0) * NM + k]));
                 fw[q] = wm;
             }
             __syncwarp();
             for (int q = lane; q < NBr * NM; q += 32) {  // (eps, b): frames (t'(b), t'(b) + T) in the window
                 const int rb = q / NM, k = q - rb * NM;
-                const int tb = NI[rb + (B0 - w.A0)].x;
+                const int tb = NI[rb].x;
                 float r = INFINITY;
                 const int f1 = min(tb + T, wend);
                 for (int f = tb + 1; f < f1; ++f) r = fminf(r, fw[(f - F0) * NM + k]);
@@ -478,8 +356,7 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
             if (lane == 0) rb = atomicAdd(&ctl->row_claim[s], 1);
             rb = __shfl_sync(0xffffffffu, rb, 0);
             if (rb >= NBr) break;
-            const int r = rb + (B0 - A0);
-            const int4 ni = NI[r];
+            const int4 ni = NI[rb];
             const int tb = ni.x, c0 = ni.y;
             const int len = min(first(tb + T), d.we) - c0;  // candidates of row b in this window (R1, R2)
             const int e0 = ni.w - w.qb0;
@@ -487,9 +364,9 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
             if (e0 < 0 || w.tb0 < 0 || w.tb0 > 3 || ly.total > caps.STAGE || e0 + len > w.qb1 - w.qb0 + 8 ||
                 c0 < B0 || c0 > w.Cend || tb < w.F0 || tb >= w.F1) {
                 if (lane == 0)
-                    printf("conv: blk %d item F[%d,%d) G[%d,%d) A0 %d B0 %d B1 %d rb %d r %d ni (%d,%d,%d,%d) qb0 %d qb1 %d "
+                    printf("conv: blk %d item F[%d,%d) G[%d,%d) A0 %d B0 %d B1 %d rb %d nA %d ni (%d,%d,%d,%d) qb0 %d qb1 %d "
                            "tb0 %d prim %d len %d lay.total %d STAGE %d tb %d\n",
-                           blockIdx.x, w.F0, w.F1, w.G0, w.G1, A0, B0, B1, rb, r, ni.x, ni.y, ni.z, ni.w, w.qb0, w.qb1,
+                           blockIdx.x, w.F0, w.F1, w.G0, w.G1, A0, B0, B1, rb, w.nA, ni.x, ni.y, ni.z, ni.w, w.qb0, w.qb1,
                            w.tb0, w.primary, len, ly.total, caps.STAGE, ly.tb);
                 continue;
             }
@@ -503,16 +380,9 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
                 const int dt = TC[w.tc0 + cc] - tb;
                 float ent[EPF];
                 if (kHasNext) ld_entry<EPF>(EN + (size_t)e * EPF, ent);  // alpha_{i+1}(c, b), landed by TMA
-                const float *u = UC + w.uc0 + cc * NM;
+                const float *u = UC + w.uc0 + cc * NM;  // lambda1 U_i(c) (K-U's scaled table)
                 const float *dl = DL + dt * NM;
-                // scalar on purpose: ptxas contracts a packed mul.rn.f32x2 feeding an add.rn.f32x2
-                // into FFMA2 (even with --fmad=false), which would change msg_n's rounding
-#pragma unroll
-                for (int k = 0; k < NM; ++k) {
-                    const float n = msg_n(kHasNext ? ent[k] : 0.f, p.l1, u[k]);
-                    mn[k] = fminf(mn[k], n);
-                    ent[k] = __fadd_rn(n, dl[k]);  // msg_m
-                }
+                msg_build<NM, kHasNext>(ent, u, dl, mn);
                 ent[NM] = TB[w.tb0 + e];  // theta(b -> c)
 #pragma unroll
                 for (int k = NM + 1; k < EPF; ++k) ent[k] = 0.f;
@@ -533,7 +403,12 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
                 if (w.primary) cur[(int64_t)(d.ntail + B0 + rb - d.wb) * EPF + lane] = fminf(bm, ean);  // (b, eps)
             }
             __syncwarp();
-            if (lane == 0) mbar_complete_tx(&ctl->conv[s], 1);
+            // release: the row's shared-memory writes (messages, b_ean) happen-before the task
+            // phase of every warp that acquires conv[s] (complete_tx itself is relaxed)
+            if (lane == 0) {
+                __threadfence_block();
+                mbar_complete_tx(&ctl->conv[s], 1);
+            }
         }
         mbar_wait(&ctl->conv[s], use & 1);  // all rows of the item are messages now
         // ---- P3: real states.  A lane task is one b with a PAIR of a's of the same a-frame
@@ -558,7 +433,7 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
                 trip = sg.trip;
             }
             const int a1 = two ? a0 + 1 : a0;
-            const int ra0 = a0 - A0, ra1 = a1 - A0, rbt = b - A0;
+            const int ra0 = a0 - A0, ra1 = a1 - A0, rbt = w.nA + (b - B0);  // row-table rows (BookPlan)
             const int colb = b - sg.f1a;  // column of b in the rows of the a-frame
             const float *erow = EN + (size_t)r_en[rbt] * EPF;
             const float *arow0 = TH + r_ofs[ra0] + sg.aoff, *arow1 = TH + r_ofs[ra1] + sg.aoff;
@@ -572,38 +447,7 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
 #pragma unroll
             for (int k = 0; k < NM; ++k) R0[k] = R1[k] = INFINITY;
             if (!__any_sync(0xffffffffu, dirty)) {
-                int j = 0;
-                for (; j + 1 < trip; j += 2) {
-                    float e0[EPF], e1[EPF];
-                    ld_entry<EPF>(erow + (size_t)j * EPF, e0);
-                    ld_entry<EPF>(erow + (size_t)(j + 1) * EPF, e1);
-                    {
-                        float v0[NM], v1[NM];
-                        cand_values<NM>(fold(e0[NM], th_ab0), fold(e0[NM], arow0[j]), e0, kc, p.l23, v0);
-                        cand_values<NM>(fold(e1[NM], th_ab0), fold(e1[NM], arow0[j + 1]), e1, kc, p.l23, v1);
-#pragma unroll
-                        for (int k = 0; k < NM; ++k) R0[k] = min3(R0[k], v0[k], v1[k]);
-                    }
-                    {
-                        float v0[NM], v1[NM];
-                        cand_values<NM>(fold(e0[NM], th_ab1), fold(e0[NM], arow1[j]), e0, kc, p.l23, v0);
-                        cand_values<NM>(fold(e1[NM], th_ab1), fold(e1[NM], arow1[j + 1]), e1, kc, p.l23, v1);
-#pragma unroll
-                        for (int k = 0; k < NM; ++k) R1[k] = min3(R1[k], v0[k], v1[k]);
-                    }
-                }
-                if (j < trip) {
-                    float e0[EPF];
-                    ld_entry<EPF>(erow + (size_t)j * EPF, e0);
-                    float v0[NM], v1[NM];
-                    cand_values<NM>(fold(e0[NM], th_ab0), fold(e0[NM], arow0[j]), e0, kc, p.l23, v0);
-                    cand_values<NM>(fold(e0[NM], th_ab1), fold(e0[NM], arow1[j]), e0, kc, p.l23, v1);
-#pragma unroll
-                    for (int k = 0; k < NM; ++k) {
-                        R0[k] = fminf(R0[k], v0[k]);
-                        R1[k] = fminf(R1[k], v1[k]);
-                    }
-                }
+                task_loop<NM, EPF>(erow, arow0, arow1, th_ab0, th_ab1, trip, kc, p.l23, R0, R1);
             } else {  // exact flag-aware loop (coincident points, R10): the padded band holds NaN
                       // for the direction of a zero-length ray, so the flags come with the angles
                 const bool co_ab0 = live && isnan(th_ab0);
@@ -712,6 +556,7 @@ __global__ void k_items(SceneView sc, const InstDesc *__restrict__ inst, int nin
             w.Cend = min(sc.first(w.F1 + T - 1), d.we);
             w.qa = __ldg(sc.qpad + w.A0);
             w.qa1 = __ldg(sc.qpad + max(sc.first(w.G1), w.A0));
+            w.nA = min(max(sc.first(w.G1), w.A0), w.B0) - w.A0;
             w.qb0 = __ldg(sc.qpad + w.B0);
             w.qb1 = __ldg(sc.qpad + w.B1);
             items[idx++] = w;
@@ -741,8 +586,8 @@ __global__ void __launch_bounds__(256) k_item_prep(SceneView sc, const WorkItem 
     const int gmin = max(1, F0 - w.G1 + 1), gmax = min(T - 1, F1 - 1 - w.G0);
     const int nseg = max(0, (F1 - F0) * (gmax - gmin + 1));
     const int th0 = w.qa & ~3;  // theta_pad index the stage's TH[0] holds (the copy starts 16-byte aligned)
-    for (int r = tid; r < w.B1 - w.A0; r += blockDim.x) {
-        const int x = w.A0 + r;
+    for (int r = tid; r < w.nA + (w.B1 - w.B0); r += blockDim.x) {
+        const int x = r < w.nA ? w.A0 + r : w.B0 + (r - w.nA);  // the a rows before B0, then the b rows
         const int4 ni = __ldg(sc.ninfo + x);  // (t', minnode(t'+1), qstart, qpad)
         r_ofs[r] = ni.w - th0;
         r_en[r] = ni.w - w.qb0;
@@ -812,18 +657,32 @@ static hgm_status launch_nm(const SceneView &v, const WorkItem *items, int nitem
                             const TileCaps &caps, cudaStream_t s) {
     const size_t smem = dp_batch_smem(caps, p.T, NM);
     auto kern = has_next ? k_dp_fused<NM, true> : k_dp_fused<NM, false>;
-    static int configured[2] = {0, 0};
-    static int blocks_per_sm[2] = {0, 0};
-    const int h = has_next ? 1 : 0;
-    if ((int)smem > configured[h]) {
-        HGM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured[h] = (int)smem;
-        HGM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[h], kern, KDP_BLOCK, smem));
-    }
-    int dev = 0, nsm = 0;
+    int dev = 0;
     HGM_CUDA(cudaGetDevice(&dev));
-    HGM_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    const int grid = std::max(1, std::min(nitems, std::max(1, blocks_per_sm[h]) * nsm));
+    // the shared-memory attribute applies per device context: cache it per device (and the
+    // occupancy it gives), under a lock -- calls on different devices / threads may race here
+    static std::mutex mu;
+    static int configured[64][2], occ[64][2], nsm_of[64];
+    int bps = 1, nsm = 0;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        const int d = dev < 0 || dev >= 64 ? 0 : dev, h = has_next ? 1 : 0;
+        if (dev < 0 || dev >= 64 || (int)smem > configured[d][h] || !nsm_of[d]) {
+            HGM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int b = 0;
+            HGM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, KDP_BLOCK, smem));
+            HGM_CUDA(cudaDeviceGetAttribute(&nsm_of[d], cudaDevAttrMultiProcessorCount, dev));
+            if (dev >= 0 && dev < 64) {
+                configured[d][h] = (int)smem;
+                occ[d][h] = b;
+            }
+            bps = b;
+        } else {
+            bps = occ[d][h];
+        }
+        nsm = nsm_of[d];
+    }
+    const int grid = std::max(1, std::min(nitems, std::max(1, bps) * nsm));
     static int traced = 0;
     unsigned long long *tbuf = nullptr;
     if (getenv("HGM_TRACE") && !traced && layer == 10) {

@@ -62,7 +62,7 @@ __device__ __forceinline__ int ns_of(const InstDesc &d) { return d.ntail + 2 * (
 struct TileCaps {  // shared-memory capacities of one K-DP work item, maxima over the call's tiles
     int NE;     // candidate entries (padded band slots of the tile's b rows)
     int TH;     // floats of the padded direction rows [A0, B1) incl. alignment slack
-    int NA;     // direction rows (a and b nodes)
+    int NA;     // row-table rows: the a rows before B0 plus the b rows
     int NB;     // b nodes
     int NC;     // candidate nodes [B0, Cend)
     int NST;    // real states
@@ -85,6 +85,8 @@ struct WorkItem {
     int G0, G1;    // a-frames [G0, G1) of the item's real states (the whole range unless T is large)
     int qa1;       // qpad[minnode(G1)]: end of the direction rows the loop reads
     int primary;   // 1: this item also finishes the b rows' dummy-form states (one item per b-tile)
+    int nA;        // row tables: the a rows [A0, A0 + nA) = [A0, min(minnode(G1), B0)), then the b rows
+                   // [B0, B1) (large T: an a-frame chunk far before its b-frame needs no rows between)
     // filled by the producer lane: shared-memory index of each range's first element
     int th0, tb0, we0, eb0, ee0, uc0, tc0, rf0, ft0, flo;
 };
@@ -94,8 +96,23 @@ constexpr int MAX_BATCH = 8;  // models of equal M evaluated together by one CTA
 // Batched layouts (NM models of equal M, model index k fastest):
 //   unary    U[((i * nn) + (n - n_lo)) * NM + k]
 //   history  hist[layer * L + off + s * SS + k]   (SS = entry_floats(NM) floats per state; v0: SS = 1)
+// K-DPW (dp_window.cu): per-window kernel, the whole recursion of one window in one CTA.
+// Entry width: NM messages + theta(b -> c), float2 for one model, whole float4s otherwise.
+__host__ __device__ constexpr int went_floats(int nm) { return nm == 1 ? 2 : entry_floats(nm); }
+struct WinCaps {  // maxima over the windows of one launch
+    int NPP;      // padded band slots of a window
+    int SW;       // window nodes
+    int W;        // window length in frames
+    int NTASK;    // task capacity (>= the tasks of every window)
+    int T;
+};
+struct WinStepPtrs {
+    const float4 *step[MAX_BATCH];  // per-model step constants (g_i, g_{i-1}, A1, K2), device
+};
+
 struct BTArgs {
-    const float *U;
+    const float *U;   // raw U (the appearance distance A)
+    const float *Us;  // lambda1 U (the recursion's values)
     int64_t nn, n_lo;
     int NM, M;
     int SS;  // floats per state in a layer (entry_floats(NM); the model index k is slot k)

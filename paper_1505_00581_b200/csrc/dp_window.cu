@@ -1,0 +1,384 @@
+// dp_window.cu -- K-DPW: the WHOLE recursion of PAPER.md Eqs. 10-11 (steps i = M..3) for
+// one window x one batch of NM models of equal M, in ONE CTA, with the window's trellis
+// resident in shared memory for all M-2 steps.
+//
+// Why: when a call has few windows (one model against one clip, C1; 50 models against
+// 60-frame blocks; one model against a whole 754-node video at T = 10; a streaming push)
+// the per-step kernel (dp_batch.cu: one launch per step, alpha layers through HBM) is
+// bound by launch latency and per-step pipeline fill, not by arithmetic -- the paper's own
+// launch-bound regime (one launch per step with a CPU sync; S = 60 blocks gave
+// identical times on three GPUs).  Its remedy was a work-group that keeps the
+// alpha row in local memory; here a CTA keeps a whole window:
+//   TH   [npp]            directions theta(a -> c) of the window's padded band rows (static)
+//   LAY  [(npp+2Sw+1)NM]  alpha layer: alpha_{i+1} at the start of step i, alpha_i at its end
+//                         (pair states in padded band order, then (b,eps), (eps,a), (eps,eps))
+//   ENT  [npp][EPF]       per candidate entry (b, c): the NM messages
+//                         m(b,c) = alpha_{i+1}(c,b) + lambda1 U_i(c) + lambda2 |g_i - (t'c - t'b)|
+//                         and theta(b -> c)
+//   UR   [Sw][NM]         the unary row U_i of the window (TMA bulk copy, prefetched a step ahead)
+//   node tables, the frame -> node table of the window, and the gap-major task list.
+// Per step: phase 1 builds the messages, the (b,eps) row minima and the dummy-form terms
+// from LAY (one warp per b row); phase 2 evaluates the real states (tasks claimed by warps:
+// a task = one b with a PAIR of a's of one frame, so each entry load serves two states;
+// longest candidate ranges first) and the dummy forms into LAY; one thread then streams
+// LAY to the alpha history in HBM with a single TMA bulk store (cp.async.bulk), which
+// overlaps the next step.  K-BT (backtrack.cu) re-evaluates its path from that history.
+//
+// The arithmetic is hgm_device.cuh's through dp_kdp.cuh's packed body (bit-identical to
+// the per-state v0 kernel and to dp_batch.cu), so the backtrack stays exact.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+
+#include "dp_kdp.cuh"
+
+namespace hgm {
+
+// 256 threads per CTA (several windows per SM); one model on few windows (fewer windows
+// than SMs, e.g. one model against a whole video) runs 1024-thread CTAs instead
+constexpr int KW_THREADS_MAX = 1024;
+
+struct WinPlan {  // shared-memory plan (byte offsets), sized by the launch's maxima
+    size_t th, ent, lay, ur, wc, bean, rmin, nt, nlo, nhi, nro, nfc, nlc, ftl, task, dl, kc, ctl, total;
+    int lay_floats;
+    __host__ __device__ WinPlan(const WinCaps &c, int NM) {
+        size_t o = 0;
+        auto take = [&](size_t bytes) {
+            const size_t r = o;
+            o = align16(o + bytes);
+            return r;
+        };
+        lay_floats = (int)(((size_t)(c.NPP + 2 * c.SW + 1) * NM + 3) & ~(size_t)3);
+        th = take(4 * (size_t)c.NPP);
+        ent = take(4 * (size_t)went_floats(NM) * c.NPP);
+        lay = take(4 * (size_t)lay_floats);
+        ur = take(4 * ((size_t)NM * c.SW + 8));
+        wc = take(4 * (size_t)NM * c.SW);
+        bean = take(4 * (size_t)NM * c.SW);
+        rmin = take(4 * (size_t)NM * c.SW);
+        nt = take(4 * (size_t)c.SW);
+        nlo = take(4 * (size_t)c.SW);
+        nhi = take(4 * (size_t)c.SW);
+        nro = take(4 * (size_t)c.SW);
+        nfc = take(4 * (size_t)c.SW);
+        nlc = take(4 * (size_t)c.SW);
+        ftl = take(4 * (size_t)(c.W + 2));
+        task = take(4 * (size_t)c.NTASK);
+        dl = take(4 * (size_t)c.T * NM);
+        kc = take(sizeof(StepConstB));
+        ctl = take(48 + 4 * (KW_THREADS_MAX / 32 + 1));
+        total = o;
+    }
+};
+
+// CTA-wide exclusive scan of one int per thread; returns the prefix, *total the sum
+template <int KW_WARPS>
+__device__ __forceinline__ int cta_excl_scan(int v, int *s_warp, int *total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int incl = warp_incl_scan(v, lane);
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const int w = lane < KW_WARPS ? s_warp[lane] : 0;
+        const int wi = warp_incl_scan(w, lane);
+        if (lane < KW_WARPS) s_warp[lane] = wi - w;
+        if (lane == KW_WARPS - 1) s_warp[KW_WARPS] = wi;
+    }
+    __syncthreads();
+    const int r = s_warp[warp] + incl - v;
+    *total = s_warp[KW_WARPS];
+    __syncthreads();
+    return r;
+}
+
+template <int NM, int KW_THREADS>
+__global__ void __launch_bounds__(KW_THREADS) k_dp_window(SceneView sc, const InstDesc *__restrict__ inst,
+                                                           float *__restrict__ hist, int64_t L, int M,
+                                                           WinStepPtrs sp, const float *__restrict__ U, int64_t nn,
+                                                           int64_t n_lo, DPParams p, WinCaps caps) {
+    constexpr int EPF = went_floats(NM);
+    constexpr int KW_WARPS = KW_THREADS / 32;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const WinPlan pl(caps, NM);
+    float *TH = reinterpret_cast<float *>(smem + pl.th);
+    float *ENT = reinterpret_cast<float *>(smem + pl.ent);
+    float *LAY = reinterpret_cast<float *>(smem + pl.lay);
+    float *UR = reinterpret_cast<float *>(smem + pl.ur);
+    float *WC = reinterpret_cast<float *>(smem + pl.wc);
+    float *BEAN = reinterpret_cast<float *>(smem + pl.bean);
+    float *RMIN = reinterpret_cast<float *>(smem + pl.rmin);
+    int *NT = reinterpret_cast<int *>(smem + pl.nt);
+    int *NLO = reinterpret_cast<int *>(smem + pl.nlo);
+    int *NHI = reinterpret_cast<int *>(smem + pl.nhi);
+    int *NRO = reinterpret_cast<int *>(smem + pl.nro);
+    int *NFC = reinterpret_cast<int *>(smem + pl.nfc);
+    int *NLC = reinterpret_cast<int *>(smem + pl.nlc);
+    int *FTL = reinterpret_cast<int *>(smem + pl.ftl);
+    unsigned *TASK = reinterpret_cast<unsigned *>(smem + pl.task);
+    float *DL = reinterpret_cast<float *>(smem + pl.dl);
+    StepConstB *s_kc = reinterpret_cast<StepConstB *>(smem + pl.kc);
+    uint64_t *ubar = reinterpret_cast<uint64_t *>(smem + pl.ctl);
+    int *s_claim = reinterpret_cast<int *>(smem + pl.ctl + 8);
+    int *s_ntask = reinterpret_cast<int *>(smem + pl.ctl + 12);
+    float *EEN = reinterpret_cast<float *>(smem + pl.ctl + 16);   // [NM] lambda1 W^d + alpha_{i+1}(eps, eps)
+    int *s_warp = reinterpret_cast<int *>(smem + pl.ctl + 48);    // KW_WARPS + 1 ints
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const InstDesc d = inst[blockIdx.x];
+    const int wb = d.wb, Sw = d.we - d.wb, npp = d.npp, T = p.T, o = d.o, W = caps.W;
+    const int EE = npp + 2 * Sw;  // (eps, eps) slot
+    const unsigned lay_bytes = (unsigned)(4 * (((size_t)(EE + 1) * NM + 3) & ~(size_t)3));
+    const int nsteps = M - 2;
+
+    if (tid == 0) {
+        mbar_init(ubar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // the unary row of the first step (i = M - 1) streams in while the tables are built
+    auto issue_u = [&](int i) {
+        Copier cl(ubar);
+        cl.range(UR, U, ((int64_t)i * nn + (wb - n_lo)) * NM, ((int64_t)i * nn + (wb - n_lo) + Sw) * NM);
+        cl.close();
+    };
+    if (tid == 0) issue_u(M - 1);
+
+    // ---- window tables (once): node info, frame -> node, direction rows
+    for (int x = tid; x < Sw; x += KW_THREADS) {
+        const int4 ni = __ldg(sc.ninfo + wb + x);  // (t', minnode(t'+1), qstart, qpad)
+        NT[x] = ni.x;
+        NLO[x] = min(ni.y, d.we) - wb;
+        NHI[x] = min(sc.first(ni.x + T), d.we) - wb;
+        NRO[x] = ni.w - d.ppad;
+        NFC[x] = __ldg(sc.rfc + wb + x);
+        NLC[x] = __ldg(sc.rlc + wb + x);
+    }
+    for (int f = tid; f <= W; f += KW_THREADS) FTL[f] = min(max(sc.first(o + f), wb), d.we) - wb;
+    for (int q = tid; q < npp; q += KW_THREADS) TH[q] = __ldg(sc.theta_pad + d.ppad + q);
+    __syncthreads();
+    // ---- task list (once): gap-major (longest candidate ranges first), per b-frame
+    // segment (b, pair of a's of frame t'(b) - g): packed b | a0 << 16 | two << 31
+    {
+        int base = 0;
+        for (int g = 1; g < T; ++g) {
+            for (int b0 = 0; b0 < Sw; b0 += KW_THREADS) {
+                const int b = b0 + tid;
+                int na = 0, a_lo = 0;
+                if (b < Sw) {
+                    const int fa = NT[b] - g - o;
+                    if (fa >= 0) {
+                        a_lo = FTL[fa];
+                        na = FTL[fa + 1] - a_lo;
+                    }
+                }
+                const int nt = (na + 1) >> 1;
+                int tot;
+                const int at = base + cta_excl_scan<KW_WARPS>(nt, s_warp, &tot);
+                for (int q = 0; q < nt; ++q) {
+                    const int a0 = a_lo + 2 * q;
+                    TASK[at + q] = (unsigned)b | ((unsigned)a0 << 16) | (a0 + 1 < a_lo + na ? 0x80000000u : 0u);
+                }
+                base += tot;
+            }
+        }
+        if (tid == 0) *s_ntask = base;
+    }
+
+    int u_use = 0;
+    for (int s = 0; s < nsteps; ++s) {
+        const int i = M - 1 - s;  // 0-based model node of this step; layer i - 2
+        const bool has_next = s > 0;
+        // ---- step constants (model gaps / angles) and the Delta table
+        if (tid == 0) {
+            StepConstB kc{};
+            for (int k = 0; k < NM; ++k) kc.c[k] = __ldg(sp.step[k] + i);
+            for (int q = 0; q < (NM + 1) / 2; ++q) {
+                const int k1 = min(2 * q + 1, NM - 1);
+                kc.nA1[q] = make_float2(-kc.c[2 * q].z, -kc.c[k1].z);
+                kc.nK2[q] = make_float2(-kc.c[2 * q].w, -kc.c[k1].w);
+            }
+            *s_kc = kc;
+            *s_claim = 0;
+        }
+        for (int q = tid; q < T * NM; q += KW_THREADS) {
+            const int dt = q / NM, k = q - dt * NM;
+            DL[q] = delta_term(p.l2, __ldg(&sp.step[k][i].x), dt);
+        }
+        mbar_wait(ubar, u_use & 1);  // U_i landed
+        ++u_use;
+        const float *Ui = UR + (((int64_t)i * nn + (wb - n_lo)) * NM & 3);
+        __syncthreads();
+        // ---- phase 1: dummy-form terms per node, messages + (b, eps) minima per row
+        for (int q = tid; q < Sw * NM; q += KW_THREADS) {
+            const int c = q / NM, k = q - c * NM;
+            WC[q] = msg_n(has_next ? LAY[(npp + c) * NM + k] : 0.f, Ui[q]);             // w(c)
+            BEAN[q] = __fadd_rn(p.l1W, has_next ? LAY[(npp + Sw + c) * NM + k] : 0.f);        // eps candidate
+        }
+        if (tid < NM) EEN[tid] = __fadd_rn(p.l1W, has_next ? LAY[EE * NM + tid] : 0.f);
+        for (int x = warp; x < Sw; x += KW_WARPS) {
+            const int c0 = NLO[x], len = NHI[x] - c0, ro = NRO[x], tx = NT[x];
+            float mn[NM];
+#pragma unroll
+            for (int k = 0; k < NM; ++k) mn[k] = INFINITY;
+            for (int j = lane; j < len; j += 32) {
+                const int c = c0 + j, e = ro + j;
+                const float *dl = DL + (NT[c] - tx) * NM;
+                float ent[EPF];
+#pragma unroll
+                for (int k = 0; k < NM; ++k) ent[k] = LAY[e * NM + k];  // alpha_{i+1}(c, x)
+                if (has_next)
+                    msg_build<NM, true>(ent, Ui + c * NM, dl, mn);
+                else
+                    msg_build<NM, false>(ent, Ui + c * NM, dl, mn);
+                ent[NM] = TH[e];
+#pragma unroll
+                for (int k = NM + 1; k < EPF; ++k) ent[k] = 0.f;
+                if constexpr (EPF % 4 == 0) {
+#pragma unroll
+                    for (int q = 0; q < EPF / 4; ++q)
+                        reinterpret_cast<float4 *>(ENT + (size_t)e * EPF)[q] =
+                            make_float4(ent[4 * q], ent[4 * q + 1], ent[4 * q + 2], ent[4 * q + 3]);
+                } else {
+                    *reinterpret_cast<float2 *>(ENT + (size_t)e * EPF) = make_float2(ent[0], ent[1]);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < NM; ++k) {  // n >= 0: float order = unsigned bit order
+                const float v = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(mn[k])));
+                if (lane == k) RMIN[x * NM + k] = v;
+            }
+        }
+        if (tid == 0) bulk_wait_read_all();  // the previous layer's bulk store has read LAY
+        __syncthreads();
+        if (tid == 0 && s + 1 < nsteps) issue_u(i - 1);  // UR is free: prefetch the next step's row
+        // ---- phase 2a: dummy-form states of step i (cheap; every thread)
+        for (int q = tid; q < Sw * NM; q += KW_THREADS) {
+            const int x = q / NM, k = q - x * NM;
+            LAY[(npp + x) * NM + k] = fminf(RMIN[q], BEAN[q]);  // (x, eps)
+            float r = INFINITY;
+            for (int c = NLO[x]; c < NHI[x]; ++c) r = fminf(r, WC[c * NM + k]);  // frames (t'x, t'x + T)
+            LAY[(npp + Sw + x) * NM + k] = fminf(r, EEN[k]);  // (eps, x)
+        }
+        if (tid < NM) LAY[EE * NM + tid] = EEN[tid];  // (eps, eps) of step i starts here ...
+        __syncthreads();
+        for (int q = tid; q < Sw * NM; q += KW_THREADS) {
+            const int k = q % NM;
+            atomicMin(reinterpret_cast<unsigned *>(LAY + EE * NM + k), __float_as_uint(WC[q]));  // ... and is min-reduced (w >= 0)
+        }
+        // ---- phase 2b: real states, 32-task groups claimed by warps
+        const StepConstB kc = *s_kc;
+        const int ntask = *s_ntask;
+        for (;;) {
+            int t0 = 0;
+            if (lane == 0) t0 = atomicAdd(s_claim, 32);
+            t0 = __shfl_sync(0xffffffffu, t0, 0);
+            if (t0 >= ntask) break;
+            const bool live = t0 + lane < ntask;
+            const unsigned tk = TASK[live ? t0 + lane : ntask - 1];
+            const int b = (int)(tk & 0xffffu), a0 = (int)((tk >> 16) & 0x7fffu);
+            const bool two = live && (tk >> 31);
+            const int a1 = two ? a0 + 1 : a0;
+            const int c0 = NLO[b], la = NLO[a0];
+            const int trip = live ? NHI[a0] - c0 : 0;
+            const int aoff = c0 - la, colb = b - la;
+            const int ra0 = NRO[a0], ra1 = NRO[a1];
+            const float *erow = ENT + (size_t)NRO[b] * EPF;
+            const float *arow0 = TH + ra0 + aoff, *arow1 = TH + ra1 + aoff;
+            const float th_ab0 = TH[ra0 + colb], th_ab1 = TH[ra1 + colb];
+            auto dirty_of = [&](int a) {
+                const int lca = NLC[a];
+                return lca >= 0 && lca >= min(colb, aoff) && NFC[a] <= max(colb, aoff + trip - 1);
+            };
+            const bool dirty = live && (dirty_of(a0) || dirty_of(a1) || NFC[b] < trip);
+            float R0[NM], R1[NM];
+#pragma unroll
+            for (int k = 0; k < NM; ++k) R0[k] = R1[k] = INFINITY;
+            if (!__any_sync(0xffffffffu, dirty)) {
+                task_loop<NM, EPF>(erow, arow0, arow1, th_ab0, th_ab1, trip, kc, p.l23, R0, R1);
+            } else {  // exact flag-aware loop (coincident points, R10): NaN directions mark them
+                const bool co_ab0 = live && isnan(th_ab0);
+                const bool co_ab1 = live && isnan(th_ab1);
+                for (int j = 0; j < trip; ++j) {
+                    float e0[EPF];
+                    ld_went<EPF>(erow + (size_t)j * EPF, e0);
+                    const bool cbc = isnan(e0[NM]);
+                    const bool cac0 = isnan(arow0[j]);
+                    const bool cac1 = isnan(arow1[j]);
+#pragma unroll
+                    for (int k = 0; k < NM; ++k) {
+                        R0[k] = fminf(R0[k], cand_value(e0[k], e0[NM], th_ab0, arow0[j], cbc || co_ab0, cbc || cac0,
+                                                        kc.c[k].z, kc.c[k].w, p.l23));
+                        R1[k] = fminf(R1[k], cand_value(e0[k], e0[NM], th_ab1, arow1[j], cbc || co_ab1, cbc || cac1,
+                                                        kc.c[k].z, kc.c[k].w, p.l23));
+                    }
+                }
+            }
+            if (live) {
+                const int g = NT[b] - NT[a0];
+#pragma unroll
+                for (int k = 0; k < NM; ++k) {
+                    const float sc_g = state_const(p.l2, kc.c[k].y, g);
+                    const float ean = BEAN[b * NM + k];
+                    LAY[(ra0 + colb) * NM + k] = fminf(__fadd_rn(R0[k], sc_g), ean);
+                    if (two) LAY[(ra1 + colb) * NM + k] = fminf(__fadd_rn(R1[k], sc_g), ean);
+                }
+            }
+        }
+        fence_async_smem();  // LAY's generic-proxy writes before the bulk store reads them
+        __syncthreads();
+        if (tid == 0) {  // alpha_i -> the history (layer i - 2), one bulk store
+            bulk_s2g(hist + (int64_t)(i - 2) * L + d.off, LAY, lay_bytes);
+            bulk_commit();
+        }
+    }
+    if (tid == 0) bulk_wait_all();
+}
+
+size_t dp_window_smem(const WinCaps &c, int NM) { return WinPlan(c, NM).total; }
+
+template <int NM, int NT>
+static hgm_status launch_w(const SceneView &v, const InstDesc *dinst, int ninst, float *hist, int64_t L, int M,
+                           const WinStepPtrs &sp, const float *U, int64_t nn, int64_t n_lo, const DPParams &p,
+                           const WinCaps &caps, cudaStream_t s) {
+    const size_t smem = dp_window_smem(caps, NM);
+    int dev = 0;
+    HGM_CUDA(cudaGetDevice(&dev));
+    static std::mutex mu;
+    static int configured[64];
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        const int d = dev < 0 || dev >= 64 ? 0 : dev;
+        if (dev < 0 || dev >= 64 || (int)smem > configured[d]) {
+            HGM_CUDA(cudaFuncSetAttribute(k_dp_window<NM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            if (dev >= 0 && dev < 64) configured[d] = (int)smem;
+        }
+    }
+    k_dp_window<NM, NT><<<ninst, NT, smem, s>>>(v, dinst, hist, L, M, sp, U, nn, n_lo, p, caps);
+    return HGM_OK;
+}
+
+hgm_status launch_dp_window(int NM, const SceneView &v, const InstDesc *dinst, int ninst, float *hist, int64_t L,
+                            int M, const WinStepPtrs &sp, const float *U, int64_t nn, int64_t n_lo,
+                            const DPParams &p, const WinCaps &caps, cudaStream_t s) {
+    if (ninst <= 0 || M < 3) return HGM_OK;
+#define HGM_NMW_CASE(n) \
+    case n: return launch_w<n, 256>(v, dinst, ninst, hist, L, M, sp, U, nn, n_lo, p, caps, s)
+    int dev = 0, nsm = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (NM == 1 && ninst < nsm) return launch_w<1, 1024>(v, dinst, ninst, hist, L, M, sp, U, nn, n_lo, p, caps, s);
+    switch (NM) {
+        HGM_NMW_CASE(1);
+        HGM_NMW_CASE(2);
+        HGM_NMW_CASE(3);
+        HGM_NMW_CASE(4);
+        HGM_NMW_CASE(5);
+        HGM_NMW_CASE(6);
+        HGM_NMW_CASE(7);
+        HGM_NMW_CASE(8);
+        default: return fail(HGM_ERR_INVALID_ARGUMENT, "model batch size must be 1..8");
+    }
+#undef HGM_NMW_CASE
+}
+
+}  // namespace hgm

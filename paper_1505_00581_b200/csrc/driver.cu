@@ -33,6 +33,10 @@ hgm_status launch_dp_v0(const SceneView &v, const InstDesc *dinst, int ninst, in
                         cudaStream_t s);
 hgm_status launch_backtrack_v0(const SceneView &v, const InstDesc *dinst, int ninst, const float *hist, int64_t L,
                                const BTArgs &bt, const DPParams &p, cudaStream_t s);
+hgm_status launch_dp_window(int NM, const SceneView &v, const InstDesc *dinst, int ninst, float *hist, int64_t L,
+                            int M, const WinStepPtrs &sp, const float *U, int64_t nn, int64_t n_lo,
+                            const DPParams &p, const WinCaps &caps, cudaStream_t s);
+size_t dp_window_smem(const WinCaps &c, int NM);
 
 static inline int host_first(const hgm_scene *sc, int64_t f) {
     if (f <= 0) return 0;
@@ -154,8 +158,9 @@ static bool make_tiling(const hgm_scene *sc, const hgm_offsets &o, int T, int NM
     }
     // stage bytes of the unclipped item: b-frames [a, b), a-frames [g0, g1)
     auto foot = [&](int64_t a, int64_t b, int64_t g0, int64_t g1, int64_t book) {
+        const int64_t nrows = std::min(NF(g1), NF(a)) - NF(g0) + (NF(b) - NF(a));  // a rows before the b rows + b rows
         return (int64_t)item_stage_bytes((int)(QP(b) - QP(a)), (int)(QP(g1) - QP(g0)), (int)(NF(b + T - 1) - NF(a)),
-                                         (int)(NF(b) - NF(g0)), (int)(NF(b) - NF(a)), (int)(b - a), T, NM, (int)book);
+                                         (int)nrows, (int)(NF(b) - NF(a)), (int)(b - a), T, NM, (int)book);
     };
     for (int bi = 0; bi < 3; ++bi) {
         TileCaps c0{1, 1, 1, 1, 1, 1, FT_max, o.window, 0, stages[bi]};
@@ -172,7 +177,7 @@ static bool make_tiling(const hgm_scene *sc, const hgm_offsets &o, int T, int NM
                 c.STAGE = (int)std::max<int64_t>(c.STAGE, foot(F0, F1, G0, G1, book));
                 c.NE = (int)std::max<int64_t>(c.NE, QP(F1) - QP(F0));
                 c.TH = (int)std::max<int64_t>(c.TH, QP(G1) - QP(G0) + 8);
-                c.NA = (int)std::max<int64_t>(c.NA, NF(F1) - NF(G0));
+                c.NA = (int)std::max<int64_t>(c.NA, std::min(NF(G1), NF(F0)) - NF(G0) + NF(F1) - NF(F0));
                 c.NB = (int)std::max<int64_t>(c.NB, NF(F1) - NF(F0));
                 c.NC = (int)std::max<int64_t>(c.NC, NF(F1 + T - 1) - NF(F0));
                 int64_t nst = 0;
@@ -231,9 +236,9 @@ static bool make_tiling(const hgm_scene *sc, const hgm_offsets &o, int T, int NM
             t.sub_begin.push_back(t.sub_begin.back());
             c.STAGE = (int)std::max<int64_t>(c.STAGE, 16);
             if (getenv("HGM_DEBUG_TILING"))  // diagnosis
-                fprintf(stderr, "tiling: budget %zu cap %lld tiles %d subs %zu STAGE %d NE %d TH %d NA %d NB %d NC %d NST %d smem %zu\n",
-                        budgets[bi], (long long)cap, ntiles, t.sub_g.size() / 2, c.STAGE, c.NE, c.TH, c.NA, c.NB, c.NC,
-                        c.NST, dp_batch_smem(c, T, NM));
+                fprintf(stderr, "tiling: NM %d budget %zu stages %d cap %lld tiles %d subs %zu STAGE %d NE %d TH %d NA %d NB %d NC %d NST %d smem %zu\n",
+                        NM, budgets[bi], stages[bi], (long long)cap, ntiles, t.sub_g.size() / 2, c.STAGE, c.NE, c.TH,
+                        c.NA, c.NB, c.NC, c.NST, dp_batch_smem(c, T, NM));
             t.caps = c;
             *tl = std::move(t);
             return true;
@@ -242,27 +247,55 @@ static bool make_tiling(const hgm_scene *sc, const hgm_offsets &o, int T, int NM
     return false;
 }
 
+// K-DPW eligibility: the largest window of the call (its padded band, nodes, task list)
+// must fit one CTA's shared memory.  Tasks per window are counted exactly from the frame
+// histogram (one task = a b with a pair of a's of one frame).  HGM_DP=fused / window
+// forces a path (the window path still needs to fit).
+static bool window_path(const hgm_scene *sc, const std::vector<InstDesc> &all, int NM, const hgm_offsets &o, int T,
+                        WinCaps *caps) {
+    const char *e = getenv("HGM_DP");
+    if (e && strcmp(e, "fused") == 0) return false;
+    WinCaps c{0, 0, o.window, 0, T};
+    for (const InstDesc &d : all) {
+        c.NPP = std::max(c.NPP, d.npp);
+        c.SW = std::max(c.SW, d.we - d.wb);
+    }
+    if (c.SW >= 32768) return false;  // tasks pack node indices in 15 / 16 bits
+    const size_t limit = 227 * 1024;
+    if (dp_window_smem(c, NM) > limit) return false;  // even without a task list
+    // tasks of the busiest window, bounded from the frame histogram: per b-frame fb,
+    // n(fb) * sum_g ceil(n(fb - g) / 2) (every gap, ignoring the clip at the window start),
+    // summed over the window's frames by a prefix sum -- O(frames x T + windows)
+    const int64_t f_lo = all.front().o, f_hi = (int64_t)all.back().o + o.window;
+    std::vector<int64_t> pre((size_t)(f_hi - f_lo) + 1, 0);
+    auto nfr = [&](int64_t f) { return (int64_t)host_first(sc, f + 1) - host_first(sc, f); };
+    for (int64_t fb = f_lo; fb < f_hi; ++fb) {
+        const int64_t nb = nfr(fb);
+        int64_t t = 0;
+        if (nb)
+            for (int g = 1; g < T; ++g) t += (nfr(fb - g) + 1) / 2;
+        pre[(size_t)(fb - f_lo) + 1] = pre[(size_t)(fb - f_lo)] + nb * t;
+    }
+    int64_t ntask_max = 0;
+    for (const InstDesc &d : all)
+        ntask_max = std::max(ntask_max, pre[(size_t)(d.o + o.window - f_lo)] - pre[(size_t)(d.o - f_lo)]);
+    c.NTASK = (int)std::max<int64_t>(1, ntask_max);
+    if (dp_window_smem(c, NM) > limit) return false;
+    *caps = c;
+    return true;
+}
+
 // Match NM models of equal chain length M at every offset.
 // U: batched unary table U[((i * nn) + (n - n_lo)) * NM + k].
 hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *sc, const hgm_params &pp,
-                       const hgm_offsets &o, const float *U, int64_t n_lo, int64_t nn, const MatchOut *outs,
-                       cudaStream_t s) {
+                       const hgm_offsets &o, const float *U, const float *Us, int64_t n_lo, int64_t nn,
+                       const MatchOut *outs, cudaStream_t s) {
     const int count = o.count, M = models[0]->M;
     if (count <= 0) return HGM_OK;
     if (NM < 1 || NM > MAX_BATCH) return fail(HGM_ERR_INVALID_ARGUMENT, "model batch size must be 1..8");
     bool v0 = use_v0_kernels();
     if (v0 && NM != 1) return fail(HGM_ERR_INVALID_ARGUMENT, "v0 kernels take one model at a time");
-    Tiling tl;
-    if (!v0 && !make_tiling(sc, o, pp.T, NM, &tl)) {
-        // a single (b-frame, a-frame) item of these frames exceeds shared memory (very
-        // dense frames at large T): a batch is retried one model at a time by the caller,
-        // and a single model falls back to the reference kernels (global-memory operands)
-        if (NM > 1) {
-            g_tiling_failed = true;
-            return fail(HGM_ERR_INVALID_ARGUMENT, "frames too dense for the shared-memory tile of a model batch");
-        }
-        v0 = true;
-    }
+    const int nsteps = M >= 3 ? M - 2 : 0;
     std::vector<InstDesc> all(count);
     for (int k = 0; k < count; ++k) {
         const int64_t of = (int64_t)o.first_frame + (int64_t)k * o.stride;
@@ -273,13 +306,32 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
         d.np = sc->qstart_h[d.we] - sc->qstart_h[d.wb];
         d.ppad = sc->qpad_h[d.wb];
         d.npp = sc->qpad_h[d.we] - sc->qpad_h[d.wb];
-        d.ntail = v0 ? d.np : d.npp;  // v0 kernels: compact pair layout
+        d.ntail = d.npp;
         d.out = k;
         d.o = (int32_t)of;
         all[k] = d;
     }
+    WinCaps wcaps{};
+    const bool win = !v0 && nsteps > 0 && window_path(sc, all, NM, o, pp.T, &wcaps);
+    if (win && getenv("HGM_DEBUG_TILING"))
+        fprintf(stderr, "window kernel: NM %d NPP %d SW %d NTASK %d smem %zu windows %d\n", NM, wcaps.NPP, wcaps.SW,
+                wcaps.NTASK, dp_window_smem(wcaps, NM), count);
+    Tiling tl;
+    if (!v0 && !win && !make_tiling(sc, o, pp.T, NM, &tl)) {
+        // a single (b-frame, a-frame) item of these frames exceeds shared memory (very
+        // dense frames at large T): a batch is retried one model at a time by the caller,
+        // and a single model falls back to the reference kernels (global-memory operands)
+        if (getenv("HGM_DEBUG_TILING")) fprintf(stderr, "tiling: NM %d does not fit%s\n", NM, NM > 1 ? "" : ": v0 fallback");
+        if (NM > 1) {
+            g_tiling_failed = true;
+            return fail(HGM_ERR_INVALID_ARGUMENT, "frames too dense for the shared-memory tile of a model batch");
+        }
+        v0 = true;
+    }
+    if (v0)
+        for (InstDesc &d : all) d.ntail = d.np;  // v0 kernels: compact pair layout
     DevBuf d_gstart, d_tile_of, d_subb, d_subg;
-    if (!v0) {
+    if (!v0 && !win) {
         HGM_TRY(d_subb.alloc(sizeof(int32_t) * tl.sub_begin.size(), s));
         HGM_TRY(d_subg.alloc(sizeof(int32_t) * std::max<size_t>(2, tl.sub_g.size()), s));
         HGM_CUDA(cudaMemcpyAsync(d_subb.p, tl.sub_begin.data(), sizeof(int32_t) * tl.sub_begin.size(),
@@ -303,18 +355,20 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
     const SceneView v{sc->t,    sc->first_tab, sc->qstart,    sc->theta,    sc->coinc, sc->cpre,
                       sc->prow, sc->id,        sc->qpad,      sc->theta_pad, sc->prow_pad, sc->rfc,
                       sc->rlc,  sc->ninfo,     sc->fmax,      (int)sc->S};
-    const int nsteps = M >= 3 ? M - 2 : 0;
     // Windows are processed in chunks (the alpha history of a chunk must fit the
     // budget; a smaller chunk keeps a layer L2-resident for the next step's reads).
     // Optionally chunks alternate between two streams.
     const int64_t budget_floats = (int64_t)3 << 29;  // alpha history per chunk: 6 GiB
     BTArgs bt{};
     bt.U = U;
+    bt.Us = Us;
     bt.nn = nn;
     bt.n_lo = n_lo;
     bt.NM = NM;
     bt.M = M;
-    const int SS = v0 ? 1 : entry_floats(NM);  // floats per state in a layer (16-byte aligned for K-DP's copies)
+    // floats per state in a layer: entry_floats(NM) for K-DP's 16-byte bulk copies, NM for
+    // K-DPW (whole layers are 16-byte aligned instead), 1 for the v0 kernels
+    const int SS = v0 ? 1 : (win ? NM : entry_floats(NM));
     bt.SS = SS;
     for (int k = 0; k < NM; ++k) {
         bt.step[k] = models[k]->step;
@@ -340,11 +394,12 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
         while (c.k1 < count && c.k1 - k0 < chunk_max) {
             InstDesc &d = all[c.k1];
             const int64_t ns = (int64_t)d.ntail + 2 * (int64_t)(d.we - d.wb) + 1;
-            if (c.k1 > k0 && (c.L + ns * SS) * std::max(nsteps, 1) > budget_floats) break;
+            const int64_t lw = win ? (ns * SS + 3) & ~(int64_t)3 : ns * SS;  // K-DPW: 16-byte aligned layers
+            if (c.k1 > k0 && (c.L + lw) * std::max(nsteps, 1) > budget_floats) break;
             d.off = c.L;
-            c.L += ns * SS;
+            c.L += lw;
             c.maxNs = std::max(c.maxNs, ns);
-            if (!v0) ibase_all[c.k1 + 1] = ibase_all[c.k1] + tl.items_of(d.o, o.window);
+            if (!v0 && !win) ibase_all[c.k1 + 1] = ibase_all[c.k1] + tl.items_of(d.o, o.window);
             ++c.k1;
         }
         c.nitems = ibase_all[c.k1] - ibase_all[k0];
@@ -376,7 +431,7 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
     DevBuf d_all, d_ibase;
     HGM_TRY(d_all.alloc(sizeof(InstDesc) * count, s));
     HGM_CUDA(cudaMemcpyAsync(d_all.p, all.data(), sizeof(InstDesc) * count, cudaMemcpyHostToDevice, s));
-    if (!v0) {
+    if (!v0 && !win) {
         HGM_TRY(d_ibase.alloc(sizeof(int32_t) * (count + 1), s));
         HGM_CUDA(cudaMemcpyAsync(d_ibase.p, ibase_all.data(), sizeof(int32_t) * (count + 1), cudaMemcpyHostToDevice, s));
     }
@@ -412,7 +467,7 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
         WorkItem *items_p = nullptr;
         int *counters_p = nullptr;
         unsigned char *book_p = nullptr;
-        if (!v0 && nsteps > 0) {
+        if (!v0 && !win && nsteps > 0) {
             const int64_t bbytes = (int64_t)item_book_bytes(tl.caps, p.T) * max_items + 16;
             if (chunk % nlanes == 0) {
                 if ((st = scr.items.ensure(sizeof(WorkItem) * max_items)) != HGM_OK) break;
@@ -449,12 +504,18 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
         // one timer around the chunk's consecutive K-DP launches (M-2 of them): nothing
         // else runs on the stream in between
         std::unique_ptr<Timer> dp_timer(nsteps > 0 ? new Timer(ls, K_DP) : nullptr);
-        for (int i = M - 1; i >= 2 && st == HGM_OK; --i) {
+        if (win && nsteps > 0) {  // K-DPW: every step of the chunk's windows in one launch
+            WinStepPtrs sp{};
+            for (int k = 0; k < NM; ++k) sp.step[k] = models[k]->step;
+            st = launch_dp_window(NM, v, di, ninst, hist, L, M, sp, Us, nn, n_lo, p, wcaps, ls);
+            count_launch(K_DP);
+        }
+        for (int i = M - 1; i >= 2 && st == HGM_OK && !win; --i) {
             const bool has_next = i + 1 <= M - 1;
             if (v0) {
                 const float4 h = models[0]->step_h[i];
                 const StepConst kc{h.x, h.y, h.z, h.w};
-                st = launch_dp_v0(v, di, ninst, maxNs, hist, L, i - 2, has_next, kc, U + (int64_t)i * nn, n_lo, p, ls);
+                st = launch_dp_v0(v, di, ninst, maxNs, hist, L, i - 2, has_next, kc, Us + (int64_t)i * nn, n_lo, p, ls);
                 count_launch(K_DP);
                 continue;
             }
@@ -466,7 +527,7 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
                 kc.nK2[q] = make_float2(-kc.c[2 * q].w, -kc.c[k1].w);
             }
             st = launch_dp_batch(NM, v, items_p, nitems, book_p, counters_p + (i - 2), hist, L, i - 2, has_next,
-                                 /*has_prev=*/i - 1 >= 2, kc, U, ((int64_t)i * nn - n_lo) * NM, p, tl.caps, ls);
+                                 /*has_prev=*/i - 1 >= 2, kc, Us, ((int64_t)i * nn - n_lo) * NM, p, tl.caps, ls);
             count_launch(K_DP);
         }
         dp_timer.reset();

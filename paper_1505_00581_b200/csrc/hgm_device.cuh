@@ -65,10 +65,12 @@ __device__ __forceinline__ float cand_value(float m_bc, float th_bc, float th_ab
     return __fmaf_rn(l23, dg_norm(fb, fc, A1, K2), m_bc);
 }
 
-// n(b,c) = alpha_{i+1}(c, b) + lambda1 * U_i(c)   (Eq. 10 without D)
-__device__ __forceinline__ float msg_n(float alpha_cb, float l1, float u_c) {
-    return __fadd_rn(alpha_cb, __fmul_rn(l1, u_c));
-}
+// n(b,c) = alpha_{i+1}(c, b) + lambda1 * U_i(c)   (Eq. 10 without D); l1u_c = lambda1 * U_i(c)
+// rounded once by K-U (unary.cu writes the scaled table next to the raw one)
+__device__ __forceinline__ float msg_n(float alpha_cb, float l1u_c) { return __fadd_rn(alpha_cb, l1u_c); }
+
+// lambda1 * U, the single rounding every kernel's scaled unary value carries
+__device__ __forceinline__ float scale_l1(float l1, float u) { return __fmul_rn(l1, u); }
 
 // lambda2 * Delta(i, i-1) for a frame gap dt = t'(c) - t'(b)
 __device__ __forceinline__ float delta_term(float l2, float g_i, int dt_cb) {

@@ -30,7 +30,8 @@ hgm_status cuda_fail(cudaError_t e, const char *what);
         if (s__ != HGM_OK) return s__;                                   \
     } while (0)
 
-constexpr int MAX_BATCH_API = 8;  // models of equal M matched together (dp_common.cuh MAX_BATCH)
+constexpr int MAX_BATCH_API = 8;
+constexpr int HGM_MAX_FRAME = 1 << 26;  // largest accepted frame index (31 days at 25 fps): bounds the frame tables  // models of equal M matched together (dp_common.cuh MAX_BATCH)
 
 // Pad descriptors to a multiple of 4 floats so rows load as float4.
 inline int pad4(int F) { return (F + 3) & ~3; }
@@ -126,8 +127,12 @@ hgm_status model_build_device(const hgm_points *dev_pts, int rank, cudaStream_t 
 
 // Unary table of a batch of NM models of M nodes each (model features stacked
 // model-major, node j = k*M + i), batched layout U[((i*nn) + (n - n_lo))*NM + k].
+// Us = lambda1 * U (same layout), the recursion's unary term
 hgm_status unary_table(const float *mfeat, int M, int NM, int Fp, const hgm_scene *sc, int64_t n_lo, int64_t n_hi,
-                       float *U, cudaStream_t s);
+                       float l1, float *U, float *Us, cudaStream_t s);
+// floats of one table of M x nn x NM (+ 16 B of K-DP bulk-copy slack), 16-byte aligned:
+// the raw table at U, the scaled one at U + unary_stride(...)
+inline int64_t unary_stride(int M, int NM, int64_t nn) { return ((int64_t)M * NM * nn + 4 + 3) & ~(int64_t)3; }
 
 struct MatchOut {  // per (model, offset) results of one model
     float *E;       // [count] device
@@ -137,8 +142,8 @@ struct MatchOut {  // per (model, offset) results of one model
 bool use_v0_kernels();
 extern thread_local bool g_tiling_failed;  // set by match_batch when a model batch must be split
 hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *sc, const hgm_params &pp,
-                       const hgm_offsets &o, const float *U, int64_t n_lo, int64_t nn, const MatchOut *outs,
-                       cudaStream_t s);
+                       const hgm_offsets &o, const float *U, const float *Us, int64_t n_lo, int64_t nn,
+                       const MatchOut *outs, cudaStream_t s);
 hgm_status offset_argmin(const float *score, int n_models, int count, float threshold, int32_t *winner,
                          float *best, cudaStream_t s);
 hgm_status chain_mean(const float *S_chain, const int32_t *chain_first, int n_models, int count, float *S_model,

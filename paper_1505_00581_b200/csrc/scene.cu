@@ -15,6 +15,8 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
+
 #include "hgm_device.cuh"
 #include "hgm_internal.cuh"
 
@@ -26,19 +28,42 @@ __global__ void k_iota(int32_t *v, int64_t n) {
 }
 
 // gather the sorted nodes; descriptors padded to Fp with zeros
+// gather the sorted nodes; descriptors padded to Fp with zeros; *bad |= 1 on a
+// non-finite coordinate or descriptor component (rejected by the caller: a NaN
+// position would read as a coincidence flag in K-DP)
 __global__ void k_gather(int64_t n, int F, int Fp, const int32_t *__restrict__ order, const int32_t *__restrict__ tk,
                          const float *__restrict__ x, const float *__restrict__ y, const float *__restrict__ feat,
-                         const int64_t *__restrict__ id, int32_t *ot, float *ox, float *oy, float *of, int64_t *oid) {
+                         const int64_t *__restrict__ id, int32_t *ot, float *ox, float *oy, float *of, int64_t *oid,
+                         int *bad) {
     int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= n) return;
     int32_t src = order[k];
     ot[k] = tk[k];
-    ox[k] = x[src];
-    oy[k] = y[src];
+    const float px = x[src], py = y[src];
+    ox[k] = px;
+    oy[k] = py;
     if (oid) oid[k] = id ? id[src] : (int64_t)src;
     const float *fr = feat + (int64_t)src * F;
     float *fo = of + k * (int64_t)Fp;
-    for (int j = 0; j < Fp; ++j) fo[j] = j < F ? fr[j] : 0.0f;
+    bool ok = isfinite(px) && isfinite(py);
+    for (int j = 0; j < Fp; ++j) {
+        const float v = j < F ? fr[j] : 0.0f;
+        ok = ok && isfinite(v);
+        fo[j] = v;
+    }
+    if (!ok) atomicOr(bad, 1);
+}
+
+// *bad |= 1 if a model point has a non-finite coordinate, saliency or descriptor component
+__global__ void k_check_finite(int64_t n, int F, const float *__restrict__ x, const float *__restrict__ y,
+                               const float *__restrict__ sal, const float *__restrict__ feat, int *bad) {
+    bool ok = true;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n * (int64_t)F;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        ok = ok && isfinite(feat[k]);
+        if (k < n) ok = ok && isfinite(x[k]) && isfinite(y[k]) && isfinite(sal[k]);  // sal never NULL here
+    }
+    if (!ok) atomicOr(bad, 1);
 }
 
 // first_tab[f] = minnode(f) for f in [0, fmax+1]; each f is written once
@@ -171,6 +196,9 @@ hgm_status scene_build_device(const hgm_points *pts, int32_t T_max, cudaStream_t
     SC_CUDA(dmalloc(&sc->feat, sizeof(float) * n * sc->Fp));
     SC_CUDA(dmalloc(&sc->id, sizeof(int64_t) * n));
     SC_CUDA(dmalloc(&sc->qstart, sizeof(int32_t) * (n + 1)));
+    DevBuf badbuf;
+    if (badbuf.alloc(sizeof(int), s) != HGM_OK) return bail(HGM_ERR_OUT_OF_MEMORY);
+    SC_CUDA(cudaMemsetAsync(badbuf.p, 0, sizeof(int), s));
     {
         DevBuf order;
         if (order.alloc(sizeof(int32_t) * n, s) != HGM_OK) return bail(HGM_ERR_OUT_OF_MEMORY);
@@ -178,21 +206,27 @@ hgm_status scene_build_device(const hgm_points *pts, int32_t T_max, cudaStream_t
         if (st != HGM_OK) return bail(st);
         unsigned g = (unsigned)((n + 255) / 256);
         k_gather<<<g, 256, 0, s>>>(n, pts->F, sc->Fp, order.as<int32_t>(), sc->t, pts->x, pts->y, pts->feat, pts->id,
-                                   sc->t, sc->x, sc->y, sc->feat, sc->id);
+                                   sc->t, sc->x, sc->y, sc->feat, sc->id, badbuf.as<int>());
         count_launch(K_SCENE);
         SC_CUDA(cudaGetLastError());
     }
-    int32_t tt[2];
+    int32_t tt[3];
     SC_CUDA(cudaMemcpyAsync(&tt[0], sc->t, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     SC_CUDA(cudaMemcpyAsync(&tt[1], sc->t + n - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SC_CUDA(cudaMemcpyAsync(&tt[2], badbuf.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     SC_CUDA(cudaStreamSynchronize(s));
     if (tt[0] < 0) return bail(fail(HGM_ERR_INVALID_ARGUMENT, "negative frame index"));
+    if (tt[1] > HGM_MAX_FRAME) return bail(fail(HGM_ERR_INVALID_ARGUMENT, "frame index above 2^26 (frames must be a video's frame numbers)"));
+    if (tt[2]) return bail(fail(HGM_ERR_INVALID_ARGUMENT, "non-finite coordinate or descriptor component"));
     sc->fmax = tt[1];
+    // T_max at or above the scene's frame span + 1 admits every pair: the band is built for
+    // min(T_max, fmax + 1), identical in result and free of int overflow in t + T
+    const int Tb = (int)std::min<int64_t>(T_max, (int64_t)sc->fmax + 1);
     SC_CUDA(dmalloc(&sc->first_tab, sizeof(int32_t) * (sc->fmax + 2 + 4)));
     k_first_tab<<<(unsigned)((n + 1 + 255) / 256), 256, 0, s>>>(n, sc->t, sc->first_tab);
     DevBuf rowlen, tmp;
     if (rowlen.alloc(sizeof(int32_t) * (n + 1), s) != HGM_OK) return bail(HGM_ERR_OUT_OF_MEMORY);
-    k_rowlen<<<(unsigned)((n + 1 + 255) / 256), 256, 0, s>>>(n, T_max, sc->fmax, sc->t, sc->first_tab,
+    k_rowlen<<<(unsigned)((n + 1 + 255) / 256), 256, 0, s>>>(n, Tb, sc->fmax, sc->t, sc->first_tab,
                                                              rowlen.as<int32_t>());
     count_launch(K_SCENE, 2);
     size_t tb = 0;
@@ -228,7 +262,7 @@ hgm_status scene_build_device(const hgm_points *pts, int32_t T_max, cudaStream_t
         SC_CUDA(dmalloc(&sc->cpre, sizeof(uint16_t) * sc->npairs));
         SC_CUDA(dmalloc(&sc->prow, sizeof(int32_t) * sc->npairs));
     }
-    k_band<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(n, T_max, sc->fmax, sc->t, sc->x, sc->y, sc->first_tab,
+    k_band<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(n, Tb, sc->fmax, sc->t, sc->x, sc->y, sc->first_tab,
                                                        sc->qstart, sc->qpad, sc->theta, sc->theta_pad, sc->coinc,
                                                        sc->cpre, sc->prow, sc->prow_pad, sc->rfc, sc->rlc);
     SC_CUDA(dmalloc(&sc->ninfo, sizeof(int4) * n));
@@ -319,15 +353,30 @@ hgm_status model_build_device(const hgm_points *pts, int rank, cudaStream_t s, h
     HGM_TRY(order.alloc(sizeof(int32_t) * n, s));
     HGM_TRY(sel.alloc(sizeof(int32_t) * n, s));
     HGM_TRY(Mdev.alloc(sizeof(int32_t), s));
+    DevBuf bad, zsal;
+    const float *sal = pts->saliency;
+    if (!sal) {  // no detector confidence given: all points equally salient (earliest wins, R-D1)
+        HGM_TRY(zsal.alloc(sizeof(float) * n, s));
+        HGM_CUDA(cudaMemsetAsync(zsal.p, 0, sizeof(float) * n, s));
+        sal = zsal.as<float>();
+    }
+    HGM_TRY(bad.alloc(sizeof(int), s));
+    HGM_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+    k_check_finite<<<(unsigned)std::min<int64_t>((n * pts->F + 255) / 256, 1024), 256, 0, s>>>(
+        n, pts->F, pts->x, pts->y, sal, pts->feat, bad.as<int>());
     HGM_TRY(sort_by_frame(pts->frame, n, keys.as<int32_t>(), order.as<int32_t>(), s));
-    k_model_select<<<1, 32, 0, s>>>(n, keys.as<int32_t>(), order.as<int32_t>(), pts->saliency, rank,
+    k_model_select<<<1, 32, 0, s>>>(n, keys.as<int32_t>(), order.as<int32_t>(), sal, rank,
                                     sel.as<int32_t>(), Mdev.as<int32_t>());
     count_launch(K_MODEL);
-    int32_t M = 0, t0 = 0;
+    int32_t M = 0, t0 = 0, t1 = 0, nbad = 0;
     HGM_CUDA(cudaMemcpyAsync(&M, Mdev.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     HGM_CUDA(cudaMemcpyAsync(&t0, keys.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    HGM_CUDA(cudaMemcpyAsync(&t1, keys.as<int32_t>() + n - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    HGM_CUDA(cudaMemcpyAsync(&nbad, bad.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     HGM_CUDA(cudaStreamSynchronize(s));
     if (t0 < 0) return fail(HGM_ERR_INVALID_ARGUMENT, "negative frame index");
+    if (t1 > HGM_MAX_FRAME) return fail(HGM_ERR_INVALID_ARGUMENT, "frame index above 2^26");
+    if (nbad) return fail(HGM_ERR_INVALID_ARGUMENT, "non-finite coordinate, saliency or descriptor component");
     if (M == 0) return fail(HGM_ERR_EMPTY_POINT_SET, "no frame has a point of this saliency rank");
     hgm_model *m = new hgm_model();
     HGM_CUDA(cudaGetDevice(&m->device));

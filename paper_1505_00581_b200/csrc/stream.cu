@@ -64,12 +64,30 @@ hgm_status hgm_stream_push(hgm_stream *st, const hgm_points *pts, int32_t n_fram
     if (n_frames < 0) return fail(HGM_ERR_INVALID_ARGUMENT, "n_frames < 0");
     *n_out = 0;
     *first_offset = st->o_next;
+    // validate everything before the stream's state changes: a failed push leaves the
+    // stream exactly as it was, so the caller can retry it (e.g. with more capacity)
     if (pts && pts->n > 0) {
         if (!pts->frame || !pts->x || !pts->y || !pts->feat) return fail(HGM_ERR_INVALID_ARGUMENT, "NULL point array");
         if (pts->F != st->F) return fail(HGM_ERR_DIMENSION_MISMATCH, "point and model descriptor lengths differ");
         for (int64_t k = 0; k < pts->n; ++k)
             if (pts->frame[k] < st->seen || pts->frame[k] >= st->seen + n_frames)
                 return fail(HGM_ERR_INVALID_ARGUMENT, "pushed point outside the pushed frames [seen, seen + n_frames)");
+    }
+    const int64_t seen1 = st->seen + n_frames;
+    const int64_t count = seen1 < st->o_next + st->window ? 0 : (seen1 - st->window - st->o_next) / st->stride + 1;
+    if (count > INT32_MAX) return fail(HGM_ERR_INVALID_ARGUMENT, "too many offsets completed by one push");
+    if (count > capacity || (count > 0 && (!winner || !score)))
+        return fail(HGM_ERR_INVALID_ARGUMENT, "output capacity below the offsets this push completes");
+    const size_t n_old = st->frame.size();
+    auto rollback = [&](hgm_status stt) {
+        st->frame.resize(n_old);
+        st->x.resize(n_old);
+        st->y.resize(n_old);
+        st->sal.resize(n_old);
+        st->feat.resize(n_old * (size_t)st->F);
+        return stt;
+    };
+    if (pts && pts->n > 0) {
         for (int64_t k = 0; k < pts->n; ++k) {
             st->frame.push_back(pts->frame[k]);
             st->x.push_back(pts->x[k]);
@@ -78,11 +96,10 @@ hgm_status hgm_stream_push(hgm_stream *st, const hgm_points *pts, int32_t n_fram
         }
         st->feat.insert(st->feat.end(), pts->feat, pts->feat + pts->n * (int64_t)st->F);
     }
-    st->seen += n_frames;
-    if (st->seen < st->o_next + st->window) return HGM_OK;
-    const int64_t count = (st->seen - st->window - st->o_next) / st->stride + 1;
-    if (count > capacity || (count > 0 && (!winner || !score)))
-        return fail(HGM_ERR_INVALID_ARGUMENT, "output capacity below the offsets this push completes");
+    if (count == 0) {
+        st->seen = seen1;
+        return HGM_OK;
+    }
     // frames rebased to base = o_next - 1; an anchor node at rebased frame 0 lies before
     // every window [1 + k * stride, ...) so it is never a label (R13), and it keeps the
     // point set non-empty through silent stretches (windows without points are valid)
@@ -100,13 +117,16 @@ hgm_status hgm_stream_push(hgm_stream *st, const hgm_points *pts, int32_t n_fram
     std::copy(st->feat.begin(), st->feat.end(), rfeat.begin() + F);
     hgm_points hp{n + 1, st->F, rf.data(), rx.data(), ry.data(), rs.data(), rfeat.data(), nullptr};
     hgm_scene *scene = nullptr;
-    HGM_TRY(hgm_build_scene_index(&hp, st->device, st->params.T, &scene));
+    hgm_status bs = hgm_build_scene_index(&hp, st->device, st->params.T, &scene);
+    if (bs != HGM_OK) return rollback(bs);
     hgm_offsets o{1, st->stride, (int32_t)count, st->window};
     const hgm_status ds = hgm_detect_actions(st->models.data(), (int32_t)st->models.size(), scene, &st->params, &o,
                                              st->score_mode, st->threshold, winner, score, nullptr, nullptr);
     hgm_free_scene(scene);
-    HGM_TRY(ds);
-    HGM_CUDA(cudaStreamSynchronize(nullptr));
+    if (ds != HGM_OK) return rollback(ds);
+    const cudaError_t se = cudaStreamSynchronize(nullptr);
+    if (se != cudaSuccess) return rollback(cuda_fail(se, "cudaStreamSynchronize(stream push)"));
+    st->seen = seen1;
     *n_out = (int32_t)count;
     st->o_next += count * st->stride;
     // drop the points no later window reads (frames < o_next)

@@ -9,10 +9,15 @@
 // and would miss the 1e-6 absolute tolerance, which is also
 // why this is not a tensor-core contraction.
 //
+// Two tables are written: U (the appearance distance A of the backtrack sums it)
+// and Us = lambda1 * U rounded once (the recursion's unary term; every K-DP / K-BT kernel
+// reads Us, so the product is formed once per (node, scene node) instead of per message).
+//
 // Layout: a CTA owns a tile of TN scene nodes and loops over model nodes in
 // tiles of TJ staged in shared memory; each thread keeps its scene node's
 // running partial sums for TJ model nodes in registers while streaming the
 // scene descriptor once per model tile (float4, L1-friendly).
+#include "hgm_device.cuh"
 #include "hgm_internal.cuh"
 
 namespace hgm {
@@ -22,7 +27,8 @@ constexpr int KU_TJ = 8;    // model nodes per register tile
 
 __global__ void __launch_bounds__(KU_TN) k_unary(const float *__restrict__ mfeat, int M, int NM, int Fp,
                                                  const float *__restrict__ sfeat, int64_t n_lo, int64_t nn,
-                                                 int tiles_per_y, float *__restrict__ U) {
+                                                 int tiles_per_y, float l1, float *__restrict__ U,
+                                                 float *__restrict__ Us) {
     const int M_total = M * NM;
     // blockIdx.y owns model-node tiles [y * tiles_per_y, (y + 1) * tiles_per_y): small
     // scenes (few scene tiles) still fill the GPU
@@ -61,15 +67,17 @@ __global__ void __launch_bounds__(KU_TN) k_unary(const float *__restrict__ mfeat
             for (int q = 0; q < KU_TJ; ++q)
                 if (q < nj) {
                     const int j = j0 + q, k = j / M, i = j - k * M;  // node j = k*M + i of model k
-                    U[((int64_t)i * nn + n) * NM + k] =
+                    const float u =
                         __fsqrt_rn(__fadd_rn(__fadd_rn(acc[q][0], acc[q][1]), __fadd_rn(acc[q][2], acc[q][3])));
+                    U[((int64_t)i * nn + n) * NM + k] = u;
+                    Us[((int64_t)i * nn + n) * NM + k] = scale_l1(l1, u);  // the recursion's lambda1 U
                 }
         }
     }
 }
 
 hgm_status unary_table(const float *mfeat, int M, int NM, int Fp, const hgm_scene *sc, int64_t n_lo, int64_t n_hi,
-                       float *U, cudaStream_t s) {
+                       float l1, float *U, float *Us, cudaStream_t s) {
     const int64_t nn = n_hi - n_lo;
     if (nn <= 0 || M * NM <= 0) return HGM_OK;
     Timer tm(s, K_UNARY);
@@ -79,7 +87,7 @@ hgm_status unary_table(const float *mfeat, int M, int NM, int Fp, const hgm_scen
     const int jt = (M * NM + KU_TJ - 1) / KU_TJ;                              // model-node tiles
     const int gy_want = (int)std::min<int64_t>(jt, std::max<int64_t>(1, (4 * 148 + gx - 1) / gx));
     const int tpy = (jt + gy_want - 1) / gy_want, gy = (jt + tpy - 1) / tpy;
-    k_unary<<<dim3((unsigned)gx, (unsigned)gy), KU_TN, smem, s>>>(mfeat, M, NM, Fp, sc->feat, n_lo, nn, tpy, U);
+    k_unary<<<dim3((unsigned)gx, (unsigned)gy), KU_TN, smem, s>>>(mfeat, M, NM, Fp, sc->feat, n_lo, nn, tpy, l1, U, Us);
     count_launch(K_UNARY);
     HGM_CUDA(cudaGetLastError());
     return HGM_OK;

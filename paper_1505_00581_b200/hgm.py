@@ -352,11 +352,14 @@ class Stream:
                                        int(score_mode), float(threshold), int(device), C.byref(h)))
         self.h = h
         self.window, self.stride = int(window), int(stride)
+        self.seen, self.o_next = 0, 0  # mirrors of the library's stream state (output sizing)
 
     def push(self, points, n_frames: int):
         """Append `points` (frames in [seen, seen + n_frames), or None) and return
-        (first_offset, winner int32[n], score float32[n]) for the completed offsets."""
-        cap = int(n_frames) // self.stride + 2
+        (first_offset, winner int32[n], score float32[n]) for the completed offsets.
+        A failed push leaves the stream unchanged."""
+        seen1 = self.seen + int(n_frames)
+        cap = max(0, (seen1 - self.window - self.o_next) // self.stride + 1) + 1  # the whole backlog
         winner = np.empty(cap, np.int32)
         score = np.empty(cap, np.float32)
         n = C.c_int32()
@@ -364,6 +367,8 @@ class Stream:
         hp = _HostPoints(points) if points is not None and points.n > 0 else None
         _check(lib().hgm_stream_push(self.h, C.byref(hp.s) if hp else None, int(n_frames), cap, winner.ctypes.data,
                                      score.ctypes.data, C.byref(n), C.byref(first)))
+        self.seen = seen1
+        self.o_next = int(first.value) + n.value * self.stride
         return int(first.value), winner[: n.value].copy(), score[: n.value].copy()
 
     def __del__(self):

@@ -29,12 +29,14 @@ class Work:
                     self.windows)
 
 
-def count_work(frames, first_frame: int, stride: int, count: int, window: int, T: int) -> Work:
+def count_work(frames, first_frame: int, stride: int, count: int, window: int, T: int,
+               per_offset: bool = False):
     """Exact counts for one model step over `count` offsets of a scene whose
-    (unsorted or sorted) integer frames are `frames`."""
+    (unsorted or sorted) integer frames are `frames`.  per_offset=True returns the
+    real-triple candidates of every offset (int64 [count]) instead of the totals."""
     frames = np.asarray(frames, dtype=np.int64)
     if count <= 0 or frames.size == 0:
-        return Work(0, 0, 0, 0, max(count, 0))
+        return np.zeros(max(count, 0), np.int64) if per_offset else Work(0, 0, 0, 0, max(count, 0))
     offs = first_frame + stride * np.arange(count, dtype=np.int64)
     lo_f = int(min(offs.min(), frames.min())) - T - 1
     hi_f = int(max(offs.max() + window, frames.max())) + T + 2
@@ -64,6 +66,8 @@ def count_work(frames, first_frame: int, stride: int, count: int, window: int, T
             st = nb * na
             rs += st
             rc += st * np.maximum(below(np.minimum(fa + T, wend)) - below(fb + 1), 0)
+    if per_offset:
+        return rc
     sw = below(wend) - below(offs)
     es = 2 * sw + 1
     ec += sw  # (eps, eps) scans the whole window

@@ -24,7 +24,10 @@ def hgm():
     return H
 
 
-def _run_and_check(H, wl, scene_idx=0, ks=None, max_ties=0.01, models=None):
+TIES = {}  # test name -> (near-ties, pairs); printed in the terminal summary (conftest.py)
+
+
+def _run_and_check(H, wl, scene_idx=0, ks=None, max_ties=0.01, models=None, tag=None):
     p = wl.params()
     scene_pts = wl.scenes[scene_idx]
     count = wl.count[scene_idx]
@@ -49,6 +52,9 @@ def _run_and_check(H, wl, scene_idx=0, ks=None, max_ties=0.01, models=None):
         elif msg:
             bad.append(msg)
     assert not bad, bad[:5]
+    if tag:
+        t0, n0 = TIES.get(tag, (0, 0))
+        TIES[tag] = (t0 + ties, n0 + len(pairs))
     assert ties <= max(1, max_ties * len(pairs)), f"{ties} near-ties of {len(pairs)}"
     return len(pairs), ties
 
@@ -56,20 +62,26 @@ def _run_and_check(H, wl, scene_idx=0, ks=None, max_ties=0.01, models=None):
 @pytest.mark.parametrize("block", range(5))
 def test_c0_seeds(hgm, block):
     """C0 tiny (M=8, ~40 points, T=5): 200 seeds per block."""
+    tag = f"C0 T=5 seeds {block * 200}-{block * 200 + 199}"
     for seed in range(block * 200, block * 200 + 200):
         wl = synth.make_workload("C0", seed=seed)
-        _run_and_check(hgm, wl, max_ties=1.0)
+        _run_and_check(hgm, wl, max_ties=1.0, tag=tag)
+    ties, n = TIES[tag]
+    assert ties <= 0.01 * n, f"{ties} near-ties in {n} C0 pairs (cap 1 %)"
 
 
 def test_c0_T10(hgm):
+    tag = "C0 T=10 seeds 0-99"
     for seed in range(100):
         wl = synth.make_workload("C0", seed=seed, T=10)
-        _run_and_check(hgm, wl, max_ties=1.0)
+        _run_and_check(hgm, wl, max_ties=1.0, tag=tag)
+    ties, n = TIES[tag]
+    assert ties <= max(1, 0.01 * n), f"{ties} near-ties in {n} C0 pairs (cap 1 %)"
 
 
 def test_c1_all_offsets(hgm):
     """C1: one M=30 model against a 600-frame clip, all 541 offsets."""
-    n, ties = _run_and_check(hgm, synth.make_workload("C1"))
+    n, ties = _run_and_check(hgm, synth.make_workload("C1"), tag="C1 all offsets")
     assert n == 541
 
 
@@ -91,6 +103,69 @@ def test_c3_sampled_short(hgm):
 def test_c4_sampled(hgm):
     wl = synth.make_workload("C4", T=10, n_frames=1200)
     _run_and_check(hgm, wl, ks=[0, 40], models=[0, 3])
+
+
+def _c4_short(T, rho, M, n_frames):
+    """C4-shaped input (W = 400, stride 10, rho, T as the stress config) with the model
+    chains cut to their first M nodes so the fp64 oracle finishes in the test budget."""
+    wl = synth.make_workload("C4", T=T, rho=rho, n_frames=n_frames)
+    cut = []
+    for m in wl.models:
+        fr = np.unique(m.frame)
+        cut.append(m.take(np.nonzero(m.frame <= fr[M - 1])[0]))
+    wl.models = cut
+    return wl
+
+
+@pytest.mark.parametrize("T,rho,M,nf,ks,cap,path", [
+    (20, 4.0, 40, 700, [0, 15, 30], None, "one-item"),    # tiles of several b-frames
+    (40, 4.0, 24, 600, [0, 20], None, "a-chunks"),        # single b-frames, a-frames in chunks
+    (80, 4.0, 12, 500, [0, 10], None, "a-chunks"),
+    (20, 8.0, 20, 600, [0, 20], None, "any"),             # densest frames
+    (80, 4.0, 12, 500, [0], "64", "single-stage"),        # one stage per CTA
+    (20, 8.0, 16, 480, [0, 8], "12", "retry"),            # batch does not fit: per-model retry + v0
+])
+def test_c4_shaped_against_oracle(hgm, capfd, monkeypatch, T, rho, M, nf, ks, cap, path):
+    """C4 stress shapes against the oracle (W=400, stride 10, T up to 80,
+    rho up to 8): every model through detect_actions (6-model batches: energies of the
+    sampled pairs) and two models through match_model_at_offsets (assignments), with
+    HGM_DEBUG_TILING confirming which tiling path ran."""
+    import torch
+
+    monkeypatch.setenv("HGM_DEBUG_TILING", "1")
+    if cap:
+        monkeypatch.setenv("HGM_SMEM_MAX_KB", cap)
+    wl = _c4_short(T, rho, M, nf)
+    p = wl.params()
+    chk = Checker(wl.models, wl.scenes[0], p, 0, wl.stride, wl.window)
+    scene = hgm.build_scene_index(wl.scenes[0], device=0, T_max=T)
+    models = [hgm.build_model_graph(m, device=0) for m in wl.models]
+    det = hgm.detect_actions(models, scene, p, 0, wl.stride, wl.count[0], wl.window, want_E_all=True,
+                             device_out=False)
+    pairs = [(m, k) for m in range(len(wl.models)) for k in ks]
+    E_o, _, A_o, z_o = chk.oracle_pairs(pairs)
+    for j, (m, k) in enumerate(pairs):
+        assert abs(float(det.E_all[m, k]) - E_o[j]) <= tol(E_o[j]), (m, k, det.E_all[m, k], E_o[j])
+    for m in (0, 3):
+        r = hgm.match_model_at_offsets(models[m], scene, p, 0, wl.stride, wl.count[0], wl.window, device_out=False)
+        for j, (mm, k) in enumerate(pairs):
+            if mm == m:
+                msg = chk.check_pair(m, k, r.E[k], r.A[k], r.z[k], E_o[j], A_o[j], z_o[j])
+                assert msg in (None, "TIE"), msg
+    torch.cuda.synchronize()
+    err = capfd.readouterr().err
+    lines = [ln for ln in err.splitlines() if ln.startswith("tiling:")]
+    assert lines, "no tiling diagnostics"
+    fits = [dict(zip(ln.split()[1::2], ln.split()[2::2])) for ln in lines if "does not fit" not in ln]
+    if path == "one-item":
+        assert any(int(f["subs"]) == int(f["tiles"]) for f in fits), lines
+    elif path == "a-chunks":
+        assert any(int(f["subs"]) > int(f["tiles"]) for f in fits), lines
+    elif path == "single-stage":
+        assert any(int(f["stages"]) == 1 for f in fits), lines
+    elif path == "retry":
+        assert any("NM 6 does not fit" in ln for ln in lines), lines
+        assert any(f["NM"] == "1" for f in fits) or any("v0 fallback" in ln for ln in lines), lines
 
 
 def test_detect_matches_oracle(hgm):
@@ -198,7 +273,8 @@ def test_device_builders_match_host_builders(hgm):
     assert torch.equal(a.E, b.E) and torch.equal(a.z, b.z)
 
 
-@pytest.mark.parametrize("name,kw", [("C1", {}), ("C2", {}), ("C3", dict(n_frames=1500)), ("C0", dict(seed=3))])
+@pytest.mark.parametrize("name,kw", [("C1", {}), ("C2", {}), ("C3", dict(n_frames=1500)), ("C0", dict(seed=3)),
+                                     ("C1", dict(T=20, rho=4.0)), ("C4", dict(T=10, n_frames=700))])
 def test_tiled_kernel_bitexact_to_reference_kernel(hgm, name, kw, monkeypatch):
     """K-DP v1 (tiled, shared memory) and K-DP v0 (one thread per state) run the
     same per-candidate arithmetic (hgm_device.cuh): results must be bit-identical."""
@@ -208,16 +284,18 @@ def test_tiled_kernel_bitexact_to_reference_kernel(hgm, name, kw, monkeypatch):
     p = wl.params()
     s = hgm.build_scene_index(wl.scenes[0], device=0, T_max=p["T"])
     out = {}
-    for kern in ("v0", "v1"):
-        monkeypatch.setenv("HGM_KERNEL", kern)
+    for kern in ("v0", "v1", "fused"):  # v1 = the default choice (per-window K-DPW when it fits)
+        monkeypatch.setenv("HGM_KERNEL", "v0" if kern == "v0" else "v1")
+        monkeypatch.setenv("HGM_DP", "fused" if kern == "fused" else "auto")
         res = []
         for mp in wl.models:
             m = hgm.build_model_graph(mp, device=0)
             res.append(hgm.match_model_at_offsets(m, s, p, wl.first[0], wl.stride, wl.count[0], wl.window))
         torch.cuda.synchronize()
         out[kern] = res
-    for a, b in zip(out["v0"], out["v1"]):
-        assert torch.equal(a.E, b.E) and torch.equal(a.A, b.A) and torch.equal(a.z, b.z)
+    for other in ("v1", "fused"):
+        for a, b in zip(out["v0"], out[other]):
+            assert torch.equal(a.E, b.E) and torch.equal(a.A, b.A) and torch.equal(a.z, b.z), other
 
 
 @pytest.mark.parametrize("name,kw", [("C2", {}), ("C3", dict(n_frames=2000)), ("C4", dict(T=10, n_frames=900)),
@@ -233,16 +311,18 @@ def test_model_batched_kernel_bitexact(hgm, name, kw, monkeypatch):
     s = hgm.build_scene_index(wl.scenes[0], device=0, T_max=p["T"])
     models = [hgm.build_model_graph(m, device=0) for m in wl.models]
     res = {}
-    for kern in ("v0", "v1"):
-        monkeypatch.setenv("HGM_KERNEL", kern)
+    for kern in ("v0", "v1", "fused"):
+        monkeypatch.setenv("HGM_KERNEL", "v0" if kern == "v0" else "v1")
+        monkeypatch.setenv("HGM_DP", "fused" if kern == "fused" else "auto")
         for mode in (0, 1):
             r = hgm.detect_actions(models, s, p, wl.first[0], wl.stride, wl.count[0], wl.window, score_mode=mode,
                                    want_E_all=True)
             torch.cuda.synchronize()
             res[(kern, mode)] = r
     for mode in (0, 1):
-        a, b = res[("v0", mode)], res[("v1", mode)]
-        assert torch.equal(a.E_all, b.E_all) and torch.equal(a.winner, b.winner) and torch.equal(a.score, b.score)
+        for other in ("v1", "fused"):
+            a, b = res[("v0", mode)], res[(other, mode)]
+            assert torch.equal(a.E_all, b.E_all) and torch.equal(a.winner, b.winner) and torch.equal(a.score, b.score)
 
 
 def test_dense_fallbacks_bitexact(hgm, monkeypatch):
@@ -370,9 +450,16 @@ def test_single_instance_unpruned(hgm, seed, plant):
     _single_check(hgm, wl, 161)
 
 
-def test_single_instance_unpruned_full_size_properties(hgm):
-    """T = +inf at the paper's full size (754 nodes): the GPU assignment is feasible, its
-    fp64 energy (oracle.energy) equals the GPU E*, and E*(inf) <= E*(80) <= E*(10)."""
+def test_single_instance_unpruned_full_size(hgm):
+    """T = +inf at the paper's full size (754 nodes, 723 frames, the
+    1853 ms row) against the oracle's result stored in tests/golden/f2_single1_Tinf.json
+    (written by tools/make_golden_f2.py, which calls only oracle/: ~2e9 candidates, ~5 min
+    on one core); plus the GPU assignment is feasible, its fp64 energy (oracle.energy)
+    equals the GPU E*, and E*(inf) <= E*(80) <= E*(10)."""
+    import json
+    import os
+
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "f2_single1_Tinf.json")))
     wl = synth.make_single(1, plant=False)
     Es = []
     for T in (10, 80, 724):
@@ -385,6 +472,13 @@ def test_single_instance_unpruned_full_size_properties(hgm):
         assert oracle.feasible(chk.models[0], win, p, zl)
         Ez = oracle.energy(chk.models[0], win, p, zl)
         assert abs(Ez - Es[-1]) <= tol(Ez), (T, Ez, Es[-1])
+        if T == 724:
+            assert gold["params"]["T"] == 724 and gold["S"] == we - wb
+            assert abs(Es[-1] - gold["E"]) <= tol(gold["E"]), (Es[-1], gold["E"])
+            if list(map(int, r.z[0])) == gold["z_ids"]:
+                assert abs(float(r.A[0]) - gold["A"]) <= tol(gold["A"])
+            else:  # near-tie rule: the GPU assignment's fp64 energy meets the bound against E*
+                assert abs(Ez - gold["E"]) <= tol(gold["E"]), (Ez, gold["E"])
     assert Es[2] <= Es[1] + tol(Es[1]) and Es[1] <= Es[0] + tol(Es[0]), Es
 
 
@@ -408,12 +502,14 @@ def test_detect_chains_matches_oracle(hgm, score_mode):
     assert cm == cm_o.tolist()
     det = hgm.detect_chains(chains, cm, len(wl.models), scene, p, 0, stride, count, 60, score_mode=score_mode,
                             want_S_all=True, device_out=False)
-    assert np.all(np.abs(det.E_all - S_o) <= 2 * tol(S_o)), np.max(np.abs(det.E_all - S_o))
+    # the model distance is a mean of chain scores, each within tol(E_chain) of the oracle;
+    # for non-negative scores the mean of those bounds is tol(mean): the bound stays tol
+    assert np.all(np.abs(det.E_all - S_o) <= tol(S_o)), np.max(np.abs(det.E_all - S_o) / tol(S_o))
     for k in range(count):
         w = int(det.winner[k])
         if w != int(w_o[k]):
-            assert abs(S_o[w, k] - S_o[w_o[k], k]) <= 2 * tol(S_o[w_o[k], k]), k
-        assert abs(float(det.score[k]) - s_o[k]) <= 2 * tol(s_o[k])
+            assert abs(S_o[w, k] - S_o[w_o[k], k]) <= tol(S_o[w_o[k], k]), k
+        assert abs(float(det.score[k]) - s_o[k]) <= tol(s_o[k])
 
 
 def test_chain_builder_errors(hgm):
@@ -495,3 +591,113 @@ def test_stream_through_silent_stretches(hgm, gap):
     r = oracle.detect(wl.models, sc_pts, p, 0, 1, count, 60, pairs=[(0, k) for k in range(gap[0], gap[1] - 60 + 1, 17)])
     for k in range(gap[0], gap[1] - 60 + 1, 17):  # empty windows: the all-dummy energy
         assert abs(s[k] - r.E[0, k]) <= 1e-6 + 1e-5 * abs(r.E[0, k])
+
+
+def test_stream_failed_push_leaves_stream_unchanged(hgm):
+    """A push whose output capacity is too small fails without consuming its frames; the
+    retried push then reports exactly what an uninterrupted stream reports."""
+    import ctypes as C
+
+    wl = synth.make_workload("C1")
+    sc = wl.scenes[0]
+    p = wl.params()
+    models = [hgm.build_model_graph(wl.models[0], device=0)]
+    ref = hgm.Stream(models, p, window=60, stride=1)
+    st = hgm.Stream(models, p, window=60, stride=1)
+    chunk = sc.take(np.nonzero(sc.frame < 100)[0])
+    hp = hgm._HostPoints(chunk)
+    n, first = C.c_int32(), C.c_int64()
+    w = np.empty(4, np.int32)
+    s = np.empty(4, np.float32)
+    status = hgm.lib().hgm_stream_push(st.h, C.byref(hp.s), 100, 4, w.ctypes.data, s.ctypes.data, C.byref(n),
+                                        C.byref(first))
+    assert status == 3 and n.value == 0  # 41 offsets complete, capacity 4
+    f0, w0, s0 = ref.push(chunk, 100)
+    f1, w1, s1 = st.push(chunk, 100)  # the same frames again: accepted, nothing was consumed
+    assert (f0, w0.tolist(), s0.tolist()) == (f1, w1.tolist(), s1.tolist()) and len(w1) == 41
+    nxt = sc.take(np.nonzero((sc.frame >= 100) & (sc.frame < 180))[0])
+    f0, w0, s0 = ref.push(nxt, 80)
+    f1, w1, s1 = st.push(nxt, 80)
+    assert (f0, w0.tolist(), s0.tolist()) == (f1, w1.tolist(), s1.tolist())
+
+
+def test_boundary_rejects_bad_points_and_clamps_T(hgm):
+    """Non-finite coordinates / descriptors / saliency and frame numbers beyond 2^26 are
+    rejected with HGM_ERR_INVALID_ARGUMENT (a NaN position would otherwise read as a
+    coincidence); T_max and T far above the scene's span give exactly the unpruned result."""
+    wl = synth.make_workload("C0", seed=4)
+    sc = wl.scenes[0]
+    for field, val in (("x", np.nan), ("y", np.inf), ("feat", np.nan)):
+        bad = sc.take(np.arange(sc.n))
+        getattr(bad, field).flat[3] = val
+        with pytest.raises(hgm.HGMError) as e:
+            hgm.build_scene_index(bad, device=0, T_max=5)
+        assert e.value.status == 3, field
+    m = wl.models[0].take(np.arange(wl.models[0].n))
+    m.saliency[0] = np.nan
+    with pytest.raises(hgm.HGMError) as e:
+        hgm.build_model_graph(m, device=0)
+    assert e.value.status == 3
+    far = sc.take(np.arange(sc.n))
+    far.frame[-1] = 1_000_000_000
+    with pytest.raises(hgm.HGMError) as e:
+        hgm.build_scene_index(far, device=0, T_max=5)
+    assert e.value.status == 3
+    p = wl.params()
+    model = hgm.build_model_graph(wl.models[0], device=0)
+    span = int(sc.frame.max()) + 1
+    ref_scene = hgm.build_scene_index(sc, device=0, T_max=span)
+    ref = hgm.match_model_at_offsets(model, ref_scene, dict(p, T=span), 0, 1, 1, wl.window, device_out=False)
+    big = hgm.build_scene_index(sc, device=0, T_max=2**31 - 1)
+    for T in (span + 1, 1_000_000, 2**31 - 1):
+        r = hgm.match_model_at_offsets(model, big, dict(p, T=T), 0, 1, 1, wl.window, device_out=False)
+        assert np.array_equal(r.E, ref.E) and np.array_equal(r.z, ref.z), T
+
+
+@pytest.mark.parametrize("case", ["context-blocks", "single-T10", "C1-detect"])
+def test_window_kernel_paths(hgm, capfd, monkeypatch, case):
+    """The per-window kernel (K-DPW: one CTA keeps a window's trellis in shared memory for
+    all M-2 steps) on the launch-bound shapes it exists for -- 50 prototypes vs 60-frame
+    blocks of the 754-node scene (8-model batches), one model vs the whole video at T=10,
+    C1 detect -- is chosen by default, and is bit-identical to the per-state v0 kernels and
+    to the per-step fused kernel; a few pairs against the oracle."""
+    import torch
+
+    monkeypatch.setenv("HGM_DEBUG_TILING", "1")
+    if case == "context-blocks":
+        ctx = synth.make_single(1, plant=False)
+        models_pts = [synth.gen_model(c, 30, 1, synth.F_KTH, "ctx-protos", s) for c in range(5) for s in range(10)]
+        scene_pts, first, stride, count, W = ctx.scenes[0], 0, 60, 12, 60
+    elif case == "single-T10":
+        ctx = synth.make_single(0, plant=True)
+        models_pts = ctx.models
+        scene_pts, first, stride, count, W = ctx.scenes[0], 0, 1, 1, ctx.window
+    else:
+        wl = synth.make_workload("C1")
+        models_pts = wl.models * 3
+        scene_pts, first, stride, count, W = wl.scenes[0], 0, 1, wl.count[0], 60
+    p = dict(lambda1=0.6, lambda2=0.2, lambda3=5.0, w_dummy=1.0, T=10)
+    scene = hgm.build_scene_index(scene_pts, device=0, T_max=10)
+    models = [hgm.build_model_graph(m, device=0) for m in models_pts]
+    res = {}
+    for kern in ("v0", "window", "fused"):
+        monkeypatch.setenv("HGM_KERNEL", "v0" if kern == "v0" else "v1")
+        monkeypatch.setenv("HGM_DP", kern if kern != "v0" else "auto")
+        r = hgm.detect_actions(models, scene, p, first, stride, count, W, want_E_all=True)
+        m0 = hgm.match_model_at_offsets(models[0], scene, p, first, stride, count, W)
+        torch.cuda.synchronize()
+        res[kern] = (r, m0)
+        err = capfd.readouterr().err
+        if kern == "window":
+            assert "window kernel:" in err, err[-2000:]
+    for other in ("window", "fused"):
+        a, b = res["v0"], res[other]
+        assert torch.equal(a[0].E_all, b[0].E_all) and torch.equal(a[0].winner, b[0].winner), other
+        assert torch.equal(a[1].E, b[1].E) and torch.equal(a[1].A, b[1].A) and torch.equal(a[1].z, b[1].z), other
+    chk = Checker(models_pts[:1], scene_pts, p, first, stride, W)
+    ks = sorted({0, count // 2, count - 1})
+    E_o, _, A_o, z_o = chk.oracle_pairs([(0, k) for k in ks])
+    m0 = res["window"][1]
+    for j, k in enumerate(ks):
+        msg = chk.check_pair(0, k, float(m0.E[k]), float(m0.A[k]), m0.z[k].cpu().numpy(), E_o[j], A_o[j], z_o[j])
+        assert msg in (None, "TIE"), msg

@@ -30,6 +30,13 @@ def test_dp_equals_exhaustive_enumeration(chunk):
         assert exhaustive.feasible(as_dict(scene), p["T"], zz), seed
         assert exhaustive.energy(as_dict(model), as_dict(scene), p, zz) == pytest.approx(Eb, rel=1e-9, abs=1e-12)
         assert Er == pytest.approx(E, rel=1e-12, abs=1e-12)  # E(z_hat) = E*
+        # appearance distance (R14): A = sum_i U(i, z_i), UNWEIGHTED by
+        # lambda1 (lambda1 is 0.6 or 1.0 here), a dummy counting W^d (Eq. 2);
+        # recomputed with the independent pure-Python Eq. 2
+        md, sd = as_dict(model), as_dict(scene)
+        A_ref = sum(exhaustive.unary(md["f"][i], None if zz[i] is None else sd["f"][zz[i]], p["w_dummy"])
+                    for i in range(len(zz)))
+        assert A == pytest.approx(A_ref, rel=1e-12, abs=1e-12), seed
         if second - Eb > 1e-9:
             assert list(z) == list(zb), seed
 
@@ -218,4 +225,20 @@ def test_empty_window_all_dummy():
     empty = scene.slice(0, 0)
     E, Er, A, z = oracle.match(model, empty, p)
     assert E == pytest.approx(p["lambda1"] * model.n * p["w_dummy"], rel=1e-15)
+    assert A == pytest.approx(model.n * p["w_dummy"], rel=1e-15)  # closed form: M W^d, not lambda1 M W^d
     assert list(z) == [-1] * model.n
+    p3 = dict(p, w_dummy=3.0, lambda1=0.6)
+    E, Er, A, z = oracle.match(model, empty, p3)
+    assert A == pytest.approx(model.n * 3.0, rel=1e-15) and E == pytest.approx(0.6 * model.n * 3.0, rel=1e-15)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_appearance_distance_C0_independent(seed):
+    """A of the oracle's assignment on C0 (F = 8, real nodes and dummies mixed by a W^d
+    that makes dummies competitive) against numpy's Eq. 2 on the returned labels."""
+    model, scene, p, _, _ = _c0(seed)
+    for wd in (0.3, 1.0):
+        pp = dict(p, w_dummy=wd)
+        E, Er, A, z = oracle.match(model, scene, pp)
+        u = [wd if z[i] < 0 else float(np.linalg.norm(model.f[i] - scene.f[z[i]])) for i in range(model.n)]
+        assert A == pytest.approx(sum(u), rel=1e-12, abs=1e-12), (seed, wd)

@@ -32,3 +32,36 @@ def test_energy_non_increasing_in_T_and_saturates():
         Es.append(oracle.detect(wl.models, wl.scenes[0], p, 0, 1, 1, wl.window).E[0, 0])
     assert all(b <= a + 1e-12 for a, b in zip(Es, Es[1:])), Es
     assert Es[-1] == Es[-2] == Es[-3]
+
+
+def test_golden_f2_unpruned_fixture_is_consistent():
+    """tests/golden/f2_single1_Tinf.json (tools/make_golden_f2.py, oracle only) holds the
+    fp64 optimum of the paper's single large instance at T = +inf: its
+    assignment is feasible, its energy recomputed from scratch by oracle.energy (Eq. 1,
+    not the DP) equals the stored E*, and A = sum of Eq. 2 over the labels (R14)."""
+    import json
+    import os
+
+    import numpy as np
+
+    import oracle
+    import synth
+
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "f2_single1_Tinf.json")))
+    wl = synth.make_single(1, plant=False)
+    model = oracle.model_nodes(wl.models[0])
+    order, scene = oracle.scene_nodes(wl.scenes[0])
+    wb, we = oracle.window_range(scene.t, 0, wl.window)
+    win = scene.slice(wb, we)
+    ids = wl.scenes[0].ids()[order]
+    pos = {int(ids[k]): k for k in range(ids.size)}
+    z = np.array([-1 if v < 0 else pos[v] - wb for v in gold["z_ids"]], np.int32)
+    p = dict(gold["params"])
+    assert gold["M"] == model.n and gold["S"] == we - wb
+    assert oracle.feasible(model, win, p, z)
+    assert abs(oracle.energy(model, win, p, z) - gold["E"]) <= 1e-9 * max(1.0, gold["E"])
+    A = sum(p["w_dummy"] if z[i] < 0 else float(np.linalg.norm(model.f[i] - win.f[z[i]])) for i in range(model.n))
+    assert abs(A - gold["A"]) <= 1e-9 * max(1.0, gold["A"])
+    # the unpruned optimum cannot exceed the T = 80 optimum (E* non-increasing in T)
+    E80 = oracle.match(model, win, dict(p, T=80))[0]
+    assert gold["E"] <= E80 + 1e-9

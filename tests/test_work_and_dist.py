@@ -9,7 +9,8 @@ import torch.multiprocessing as mp
 
 import oracle
 import synth
-from paper_1505_00581_b200.dist import detect_actions_sharded, pack_keys, shard_offsets, unpack_keys
+from paper_1505_00581_b200.dist import (balanced_cuts, detect_actions_sharded, grid_shape, offset_work, pack_keys,
+                                        shard_offsets, unpack_keys)
 from paper_1505_00581_b200.work import count_work
 
 
@@ -71,6 +72,78 @@ def test_shards_cover_offsets_contiguously():
         assert sh[0].k_begin == 0 and sh[-1].k_end == 541
         for a, b in zip(sh, sh[1:]):
             assert a.k_end == b.k_begin
+
+
+def test_shards_balanced_by_predicted_work():
+    """Offset ranges are balanced by the exact per-offset candidate counts for every
+    count (no uniform fallback), and the per-offset counts sum to the total."""
+    wl = synth.make_workload("C3", n_frames=6000)
+    fr = wl.scenes[0].frame
+    count = wl.count[0]
+    per = offset_work(fr, 0, 1, count, 60, 10)
+    assert int((per - 1).sum()) == count_work(fr, 0, 1, count, 60, 10).real_candidates
+    for world in (2, 3, 8):
+        sh = shard_offsets(fr, 0, 1, count, 60, 10, world)
+        loads = [per[s.k_begin:s.k_end].sum() for s in sh]
+        assert max(loads) <= per.sum() / world + per.max() + 1e-9, (world, loads)
+        assert all(s.m_end is None for s in sh)  # count >= world x 148: offsets only
+
+
+def test_grid_shape_and_model_cuts():
+    assert grid_shape(8, 24941, 6) == (8, 1)      # C3: offsets fill the SMs
+    assert grid_shape(8, 361, 6) == (4, 2)        # C4: 361 offsets < 8 x 148: 3 models x 91 offsets
+    assert grid_shape(4, 541, 1) == (4, 1)        # one model: nothing to split
+    assert grid_shape(2, 100, 6) == (2, 1)        # equal blocks: keep 6-model batches
+    assert grid_shape(4, 2, 5) == (2, 2)          # both axes
+    assert grid_shape(2, 1, 50) == (1, 2)         # one window, 50 models (the paper's context)
+    assert balanced_cuts([1, 1, 1, 1], 2) == [0, 2, 4]
+    assert balanced_cuts([10, 1, 1, 1], 2) == [0, 1, 4]
+    wl = synth.make_workload("C4", T=10)
+    sh = shard_offsets(wl.scenes[0].frame, 0, 10, wl.count[0], 400, 10, 8, model_sizes=[200] * 6)
+    assert {(s.m_begin, s.m_end) for s in sh} == {(0, 3), (3, 6)}
+    assert sorted({(s.k_begin, s.k_end) for s in sh})[0][0] == 0
+
+
+def _fake_compute(models_pts, scene_pts, params, first_frame, stride, count, window, score_mode, threshold):
+    """A deterministic stand-in for the per-rank compute: score of (model, offset) is a
+    function of the model's points and the offset's absolute first frame only, with
+    frequent exact ties between models (the lowest index must win)."""
+    offs = first_frame + stride * np.arange(count)
+    S = np.stack([((offs * 7 + int(m.x.sum()) * 3) % 11).astype(np.float32) for m in models_pts])
+    return S.min(axis=0), S.argmin(axis=0).astype(np.int32)
+
+
+def _fake_worker(rank, world, port, count, out):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    wl = synth.make_workload("C1")
+    models = [synth.gen_model(c, 30, 2, synth.F_KTH, "dist-fake", 0) for c in range(5)]
+    w, s = detect_actions_sharded(models, wl.scenes[0], wl.params(), 3, 1, count, 60, compute=_fake_compute)
+    out[rank] = (w.tolist(), s.tolist())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,count", [(2, 1), (4, 2), (3, 2), (2, 40), (3, 500), (4, 541)])
+def test_sharded_grid_equals_single_process_gloo(world, count):
+    """Both axes (offset ranges, model ranges with all_reduce(MIN) of packed keys) and
+    the offset-only all_gather path give exactly the single-process argmin."""
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_fake_worker, args=(r, world, port, count, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    wl = synth.make_workload("C1")
+    models = [synth.gen_model(c, 30, 2, synth.F_KTH, "dist-fake", 0) for c in range(5)]
+    s_ref, w_ref = _fake_compute(models, wl.scenes[0], None, 3, 1, count, 60, 0, None)
+    for r in range(world):
+        w, s = out[r]
+        assert w == w_ref.tolist() and s == s_ref.tolist()
 
 
 def _oracle_compute(models_pts, scene_pts, params, first_frame, stride, count, window, score_mode, threshold):

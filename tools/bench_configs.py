@@ -24,7 +24,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--steps", type=int, default=5)
 ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--only", default="")
+ap.add_argument("--dp", default="", help="force the K-DP path: fused | window (default: the library's choice)")
 a = ap.parse_args()
+if a.dp:
+    import os
+
+    os.environ["HGM_DP"] = a.dp
 
 
 def sm_clock():
@@ -54,6 +59,9 @@ def rows():
     p = ctx.params()
     yield "context: 50 models x 754-node scene, W=stride=60", protos, ctx.scenes, 60, 12, 60, p
     yield "context: 50 models x 754-node scene, W=723", protos, ctx.scenes, 1, 1, 723, p
+    sg = synth.make_single(0, plant=True)
+    yield "f2 single instance 754 nodes, T=10", sg.models, sg.scenes, 1, 1, 723, sg.params()
+    yield "f2 single instance 754 nodes, T=inf", sg.models, sg.scenes, 1, 1, 723, dict(sg.params(), T=724)
 
 
 for name, models_pts, scenes_pts, stride, count, W, p in rows():
@@ -90,7 +98,7 @@ for name, models_pts, scenes_pts, stride, count, W, p in rows():
     pairs = len(models) * count * len(scenes)
     roof = 148 * 128 * f * 1e6 / ISSUE_SLOTS_PER_CAND / 1e9
     ach = cand / (dp_ms / 1e3) / 1e9 if dp_ms > 0 else 0.0
-    print(json.dumps(dict(config=name, pairs=pairs, ms_per_call=round(ms, 4), pairs_per_s=round(pairs / ms * 1e3, 1),
+    print(json.dumps(dict(config=name, dp_path=a.dp or "auto", pairs=pairs, ms_per_call=round(ms, 4), pairs_per_s=round(pairs / ms * 1e3, 1),
                           dp_ms=round(dp_ms, 4), dp_share=round(dp_ms / ms, 3), real_candidates=int(cand),
                           dp_gcand_s=round(ach, 1), roofline_gcand_s=round(roof, 1), frac=round(ach / roof, 4),
                           frac_wall=round(cand / (ms / 1e3) / 1e9 / roof, 4),
