@@ -13,6 +13,13 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "lib", "libhgm.so")
 OBJ = os.path.join(HERE, "lib", "obj")
+# A/B builds (tools only): HGM_BUILD_DEFS="-DX=1 ..." and HGM_BUILD_TAG=name write
+# lib/libhgm_<name>.so (load it with HGM_LIB); the product build is the default one.
+_DEFS = os.environ.get("HGM_BUILD_DEFS", "").split()
+_TAG = os.environ.get("HGM_BUILD_TAG", "")
+if _TAG:
+    OUT = os.path.join(HERE, "lib", f"libhgm_{_TAG}.so")
+    OBJ = os.path.join(HERE, "lib", f"obj_{_TAG}")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr"]
@@ -41,7 +48,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 and os.path.getmtime(obj) >= max(hdr_time, os.path.getmtime(src))):
             return obj
         tmp = obj + f".tmp{os.getpid()}"
-        subprocess.check_call([NVCC, *ARCH, *FLAGS, *extra, "-c", src, "-o", tmp])
+        subprocess.check_call([NVCC, *ARCH, *FLAGS, *_DEFS, *extra, "-c", src, "-o", tmp])
         os.replace(tmp, obj)
         return obj
 

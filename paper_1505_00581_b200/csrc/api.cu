@@ -411,29 +411,23 @@ hgm_status hgm_match_model_at_offsets(const hgm_model *model, const hgm_scene *s
     return HGM_OK;
 }
 
-// E* and A of every (model, offset) into device matrices Ed / Ad [n_models][count].
-static hgm_status detect_scores(const hgm_model *const *models, int32_t n_models, const hgm_scene *scene,
-                                const hgm_params *params, const hgm_offsets *offsets, float *Ed, float *Ad,
-                                cudaStream_t s) {
-    const int count = offsets->count;
-    configure_pool();
-    int64_t n_lo, n_hi;
-    covered_range(scene, offsets, &n_lo, &n_hi);
+// One model batch [m0, m1) of equal chain length on stream s (lane: its K-DP scratch set),
+// E* / A into Ed / Ad [n_models][count], assignments into the scratch zb.  A batch too
+// dense for a shared stage (g_tiling_failed) is retried one model at a time.
+static hgm_status run_batch(const hgm_model *const *models, int m0, int m1, const hgm_scene *scene,
+                            const hgm_params *params, const hgm_offsets *offsets, int64_t n_lo, int64_t n_hi,
+                            float *Ed, float *Ad, int64_t *zb, int Mmax, cudaStream_t s, int lane) {
+    const int count = offsets->count, Fp = scene->Fp;
     const int64_t nn = std::max<int64_t>(n_hi - n_lo, 1);
-    const int Fp = scene->Fp;
-    DevBuf mfeat, U, zb;
-    int Mmax = 0;
-    for (int m = 0; m < n_models; ++m) Mmax = std::max(Mmax, models[m]->M);
-    HGM_TRY(zb.alloc(sizeof(int64_t) * (size_t)count * Mmax * MAX_BATCH_API, s));
-    // batches of consecutive models with equal chain length share one K-DP pass
-    int max_batch = use_v0_kernels() ? 1 : MAX_BATCH_API;
-    for (int m0 = 0; m0 < n_models;) {
-        int m1 = m0 + 1;
-        while (m1 < n_models && m1 - m0 < max_batch && models[m1]->M == models[m0]->M) ++m1;
-        const int NM = m1 - m0, M = models[m0]->M;
+    const hgm_params pe = effective_params(params, scene);
+    int max_batch = m1 - m0;
+    for (int a = m0; a < m1;) {
+        const int b = std::min(m1, a + max_batch);
+        const int NM = b - a, M = models[a]->M;
+        DevBuf mfeat, U;
         HGM_TRY(mfeat.alloc(sizeof(float) * (size_t)NM * M * Fp, s));
         for (int k = 0; k < NM; ++k)
-            HGM_CUDA(cudaMemcpyAsync(mfeat.as<float>() + (size_t)k * M * Fp, models[m0 + k]->feat,
+            HGM_CUDA(cudaMemcpyAsync(mfeat.as<float>() + (size_t)k * M * Fp, models[a + k]->feat,
                                      sizeof(float) * (size_t)M * Fp, cudaMemcpyDeviceToDevice, s));
         const int64_t ustr = unary_stride(M, NM, nn);  // raw U, then lambda1 U
         HGM_TRY(U.alloc(sizeof(float) * 2 * (size_t)ustr, s));
@@ -441,20 +435,76 @@ static hgm_status detect_scores(const hgm_model *const *models, int32_t n_models
                             U.as<float>() + ustr, s));
         MatchOut mo[MAX_BATCH_API];
         for (int k = 0; k < NM; ++k)
-            mo[k] = MatchOut{Ed + (size_t)(m0 + k) * count, Ad + (size_t)(m0 + k) * count,
-                             zb.as<int64_t>() + (size_t)k * count * Mmax};
+            mo[k] = MatchOut{Ed + (size_t)(a + k) * count, Ad + (size_t)(a + k) * count, zb + (size_t)k * count * Mmax};
         g_tiling_failed = false;
-        const hgm_params pe = effective_params(params, scene);
         const hgm_status bst =
-            match_batch(models + m0, NM, scene, pe, *offsets, U.as<float>(), U.as<float>() + ustr, n_lo, nn, mo, s);
+            match_batch(models + a, NM, scene, pe, *offsets, U.as<float>(), U.as<float>() + ustr, n_lo, nn, mo, s, lane);
         if (bst != HGM_OK && g_tiling_failed && NM > 1) {
             if (getenv("HGM_DEBUG_TILING")) fprintf(stderr, "tiling: batch of %d retried one model at a time\n", NM);
             max_batch = 1;  // too dense for a batch's stage: one model at a time from here on
-            m1 = m0;
             continue;
         }
         HGM_TRY(bst);
+        a = b;
+    }
+    return HGM_OK;
+}
+
+// E* and A of every (model, offset) into device matrices Ed / Ad [n_models][count].
+// Consecutive models of equal chain length form batches of up to MAX_BATCH_API (one K-DP
+// pass each).  When the call has few windows (count < 2 x SMs: one batch cannot fill the
+// GPU -- the paper's context of 50 models against 60-frame blocks, streaming pushes) the
+// batches run CONCURRENTLY, one lane (stream + scratch set) each, forked from and joined
+// back into the caller's stream; otherwise one after another on it.
+static hgm_status detect_scores(const hgm_model *const *models, int32_t n_models, const hgm_scene *scene,
+                                const hgm_params *params, const hgm_offsets *offsets, float *Ed, float *Ad,
+                                cudaStream_t s) {
+    const int count = offsets->count;
+    configure_pool();
+    int64_t n_lo, n_hi;
+    covered_range(scene, offsets, &n_lo, &n_hi);
+    int Mmax = 0;
+    for (int m = 0; m < n_models; ++m) Mmax = std::max(Mmax, models[m]->M);
+    const int max_batch = use_v0_kernels() ? 1 : MAX_BATCH_API;
+    std::vector<std::pair<int, int>> batches;
+    for (int m0 = 0; m0 < n_models;) {
+        int m1 = m0 + 1;
+        while (m1 < n_models && m1 - m0 < max_batch && models[m1]->M == models[m0]->M) ++m1;
+        batches.emplace_back(m0, m1);
         m0 = m1;
+    }
+    const int nb = (int)batches.size();
+    int nsm = 148;
+    HGM_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, scene->device));
+    const char *lenv = getenv("HGM_LANES");  // 1: batches one after another (tuning / tests)
+    int nlane = (nb > 1 && !use_v0_kernels() && count < 2 * nsm) ? std::min(nb, MAX_LANES) : 1;
+    if (lenv && atoi(lenv) >= 1) nlane = std::min({nb, MAX_LANES, atoi(lenv)});
+    DevBuf zb;
+    const size_t zlane = (size_t)count * Mmax * MAX_BATCH_API;
+    HGM_TRY(zb.alloc(sizeof(int64_t) * zlane * nlane, s));
+    if (nlane == 1) {
+        for (const auto &b : batches)
+            HGM_TRY(run_batch(models, b.first, b.second, scene, params, offsets, n_lo, n_hi, Ed, Ad, zb.as<int64_t>(),
+                              Mmax, s, 0));
+    } else {
+        cudaEvent_t fork = nullptr, join[MAX_LANES] = {};
+        HGM_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+        HGM_CUDA(cudaEventRecord(fork, s));
+        hgm_status st = HGM_OK;
+        for (int l = 0; l < nlane; ++l) HGM_CUDA(cudaStreamWaitEvent(aux_stream(scene->device, 1 + l), fork, 0));
+        for (int bi = 0; bi < nb && st == HGM_OK; ++bi) {
+            const int l = bi % nlane;
+            st = run_batch(models, batches[bi].first, batches[bi].second, scene, params, offsets, n_lo, n_hi, Ed, Ad,
+                           zb.as<int64_t>() + zlane * l, Mmax, aux_stream(scene->device, 1 + l), 1 + l);
+        }
+        for (int l = 0; l < nlane; ++l) {  // join (also after a failure: nothing may outlive the call's buffers)
+            cudaEventCreateWithFlags(&join[l], cudaEventDisableTiming);
+            cudaEventRecord(join[l], aux_stream(scene->device, 1 + l));
+            cudaStreamWaitEvent(s, join[l], 0);
+            cudaEventDestroy(join[l]);
+        }
+        cudaEventDestroy(fork);
+        HGM_TRY(st);
     }
     scene->uses.record(s);
     for (int m = 0; m < n_models; ++m) models[m]->uses.record(s);

@@ -29,8 +29,8 @@
 // lambda1 U and the Delta table give the NM messages of every candidate entry,
 // stored with theta(b -> c) as float4s; the (b, eps) minimum is a full-warp
 // redux), the dummy-form states; then the next item's copies are issued; P3 the
-// state -> segment map; P4 the real states, one per lane, ordered by frame gap so
-// the lanes of a warp see near-equal trip counts.  Per candidate: 2 LDS.128
+// state -> segment map; P4 the real states, one per lane, segments in descending
+// order of their trip counts so the lanes of a warp see near-equal trips.  Per candidate: 2 LDS.128
 // (messages + theta_bc), 1 LDS (theta_ac), the two scene-angle folds shared by the
 // NM models, then per PAIR of models FADD2, FADD2, FMUL2, FFMA2, 2 MUFU.SQRT, FFMA2
 // (packed f32x2, sm_100) and a 3-input min over candidate pairs.  States touching a
@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
         mbar_wait(&ctl->conv[s], use & 1);  // all rows of the item are messages now
         // ---- P3: real states.  A lane task is one b with a PAIR of a's of the same a-frame
         // (same candidate range), so each candidate entry (b, c_j) is loaded once for two
-        // states; warps claim 32-task groups (gap-major order: longest trips first).
+        // states; warps claim 32-task groups (segments by descending trip count).
         for (;;) {
             int s0 = 0;
             if (lane == 0) s0 = atomicAdd(&ctl->task_claim[s], 32);
@@ -567,7 +567,7 @@ __global__ void k_items(SceneView sc, const InstDesc *__restrict__ inst, int nin
 // Step-independent bookkeeping of every work item of a chunk (one CTA per item):
 // the segment table of its real states (a (b-frame, a-frame) segment shares its
 // candidate range [minnode(t'(b)+1), minnode(t'(a)+T))) in
-// gap-major order with prefix starts, the state -> segment map, and the row tables.
+// descending trip order with prefix starts, the state -> segment map, and the row tables.
 __global__ void __launch_bounds__(256) k_item_prep(SceneView sc, const WorkItem *__restrict__ items, TileCaps caps,
                                                    int T, unsigned char *__restrict__ book) {
     const BookPlan bp(caps, T);
@@ -596,9 +596,10 @@ __global__ void __launch_bounds__(256) k_item_prep(SceneView sc, const WorkItem 
         r_fc[r] = __ldg(sc.rfc + x);  // whole (unclipped) row: conservative
         r_lc[r] = __ldg(sc.rlc + x);
     }
+    __shared__ int s_key[256];
     Seg sg{};
     int cnt = 0;
-    if (tid < nseg) {  // segments, gap-major: long candidate ranges first
+    if (tid < nseg) {  // segments (enumerated gap-major), then ordered by candidate count below
         const int g = gmin + tid / (F1 - F0);
         const int f = F0 + tid % (F1 - F0);
         if (f - g >= w.d.o && f - g >= w.G0 && f - g < w.G1) {
@@ -614,7 +615,19 @@ __global__ void __launch_bounds__(256) k_item_prep(SceneView sc, const WorkItem 
             cnt = sg.nb * ((sg.f1a - sg.a0 + 1) >> 1);  // lane tasks: one b, a pair of a's
         }
     }
-    s_cnt[tid] = cnt;
+    // rank = position in descending trip order (ties: enumeration order), so the 32 lanes of
+    // a task group see near-equal trip counts (warp lanes idle less at the end of the loop)
+    s_key[tid] = (tid < nseg && cnt > 0) ? sg.trip : -1;
+    __syncthreads();
+    int rank = 0;
+    if (tid < nseg) {
+        const int key = s_key[tid];
+        for (int j = 0; j < nseg; ++j) {
+            const int kj = s_key[j];
+            rank += (kj > key || (kj == key && j < tid)) ? 1 : 0;
+        }
+    }
+    if (tid < nseg) s_cnt[rank] = cnt;
     __syncthreads();
     if (warp == 0) {  // prefix over the segments (nseg <= 255)
         int carry = 0;
@@ -628,9 +641,9 @@ __global__ void __launch_bounds__(256) k_item_prep(SceneView sc, const WorkItem 
     }
     __syncthreads();
     if (tid < nseg) {
-        sg.start = s_cnt[tid];
-        seg[tid] = sg;
-        for (int q = 0; q < cnt; ++q) smap[sg.start + q] = (uint8_t)tid;
+        sg.start = s_cnt[rank];
+        seg[rank] = sg;
+        for (int q = 0; q < cnt; ++q) smap[sg.start + q] = (uint8_t)rank;
     }
 }
 

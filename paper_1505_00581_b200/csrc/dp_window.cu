@@ -35,8 +35,7 @@
 
 namespace hgm {
 
-// 256 threads per CTA (several windows per SM); one model on few windows (fewer windows
-// than SMs, e.g. one model against a whole video) runs 1024-thread CTAs instead
+// 256, 512 or 1024 threads per CTA (launch_nm_w: ~32 warps per SM)
 constexpr int KW_THREADS_MAX = 1024;
 
 struct WinPlan {  // shared-memory plan (byte offsets), sized by the launch's maxima
@@ -358,15 +357,39 @@ static hgm_status launch_w(const SceneView &v, const InstDesc *dinst, int ninst,
     return HGM_OK;
 }
 
+// CTA size: a window's steps are serial, so the warps of an SM are what hides the
+// latencies of its phases.  Shared memory bounds the CTAs per SM (k, the window's trellis
+// is resident); the CTA size is chosen so that k CTAs bring ~32 warps per SM -- 1024
+// threads when one window fills an SM's shared memory (C1: 147 KB) or the launch has fewer
+// windows than SMs, 512 at two per SM, else 256.  Register budgets cap it: 1024-thread
+// CTAs only for NM <= 2 (64 registers per thread), 512 otherwise.
+template <int NM>
+static hgm_status launch_nm_w(const SceneView &v, const InstDesc *dinst, int ninst, float *hist, int64_t L, int M,
+                              const WinStepPtrs &sp, const float *U, int64_t nn, int64_t n_lo, const DPParams &p,
+                              const WinCaps &caps, cudaStream_t s, int nsm, int smem_sm) {
+    const size_t smem = dp_window_smem(caps, NM);
+    const int per_sm = std::max(1, smem_sm / (int)(smem + 1024));  // CTAs per SM by shared memory
+    const int k = ninst < nsm ? 1 : std::min(per_sm, (ninst + nsm - 1) / nsm);
+    int nt = k <= 1 ? 1024 : (k == 2 ? 512 : 256);
+    if (const char *e = getenv("HGM_WIN_THREADS")) nt = atoi(e);  // tuning knob
+    if constexpr (NM <= 2) {
+        if (nt >= 1024) return launch_w<NM, 1024>(v, dinst, ninst, hist, L, M, sp, U, nn, n_lo, p, caps, s);
+    }
+    if (nt >= 512) return launch_w<NM, 512>(v, dinst, ninst, hist, L, M, sp, U, nn, n_lo, p, caps, s);
+    return launch_w<NM, 256>(v, dinst, ninst, hist, L, M, sp, U, nn, n_lo, p, caps, s);
+}
+
 hgm_status launch_dp_window(int NM, const SceneView &v, const InstDesc *dinst, int ninst, float *hist, int64_t L,
                             int M, const WinStepPtrs &sp, const float *U, int64_t nn, int64_t n_lo,
                             const DPParams &p, const WinCaps &caps, cudaStream_t s) {
     if (ninst <= 0 || M < 3) return HGM_OK;
+    int dev = 0, nsm = 148, smem_sm = 228 * 1024;
+    if (cudaGetDevice(&dev) == cudaSuccess) {
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    }
 #define HGM_NMW_CASE(n) \
-    case n: return launch_w<n, 256>(v, dinst, ninst, hist, L, M, sp, U, nn, n_lo, p, caps, s)
-    int dev = 0, nsm = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (NM == 1 && ninst < nsm) return launch_w<1, 1024>(v, dinst, ninst, hist, L, M, sp, U, nn, n_lo, p, caps, s);
+    case n: return launch_nm_w<n>(v, dinst, ninst, hist, L, M, sp, U, nn, n_lo, p, caps, s, nsm, smem_sm)
     switch (NM) {
         HGM_NMW_CASE(1);
         HGM_NMW_CASE(2);

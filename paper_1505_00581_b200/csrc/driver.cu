@@ -44,14 +44,16 @@ static inline int host_first(const hgm_scene *sc, int64_t f) {
     return sc->first_h[f];
 }
 
-// second stream of the chunk pipeline, one per device
-static cudaStream_t aux_stream(int device) {
+// extra streams per device: index 0 = the second lane of the chunk pipeline, 1.. = the
+// lanes of concurrent model batches (detect_scores)
+constexpr int N_AUX = 1 + MAX_LANES;
+cudaStream_t aux_stream(int device, int idx) {
     static std::mutex mu;
-    static cudaStream_t as[64] = {};
+    static cudaStream_t as[64][N_AUX] = {};
     std::lock_guard<std::mutex> lk(mu);
-    if (device < 0 || device >= 64) return nullptr;
-    if (!as[device]) cudaStreamCreateWithFlags(&as[device], cudaStreamNonBlocking);
-    return as[device];
+    if (device < 0 || device >= 64 || idx < 0 || idx >= N_AUX) return nullptr;
+    if (!as[device][idx]) cudaStreamCreateWithFlags(&as[device][idx], cudaStreamNonBlocking);
+    return as[device][idx];
 }
 
 // Per-device cache of K-DP's large scratch buffers (alpha history, work items, item
@@ -87,13 +89,16 @@ struct ScratchSet {
     Scratch hist, items, book, counters;
     cudaEvent_t done = nullptr;
 };
-static ScratchSet &scratch_set(int device) {
+// one set per (device, lane): lane 0 serves single-batch calls, lanes 1.. the concurrent
+// model batches of a detect call (each lane is one stream, so its set is never shared)
+static ScratchSet &scratch_set(int device, int lane) {
     static std::mutex mu;
-    static ScratchSet *sets[64] = {};
+    static ScratchSet *sets[64][MAX_LANES + 1] = {};
     std::lock_guard<std::mutex> lk(mu);
     const int d = device < 0 || device >= 64 ? 0 : device;
-    if (!sets[d]) sets[d] = new ScratchSet();
-    return *sets[d];
+    const int l = lane < 0 || lane > MAX_LANES ? 0 : lane;
+    if (!sets[d][l]) sets[d][l] = new ScratchSet();
+    return *sets[d][l];
 }
 
 thread_local bool g_tiling_failed = false;
@@ -148,6 +153,8 @@ static bool make_tiling(const hgm_scene *sc, const hgm_offsets &o, int T, int NM
     if (const char *menv = getenv("HGM_SMEM_MAX_KB"))  // testing: cap every budget (forces the fallbacks)
         for (size_t &b : budgets) b = std::min(b, (size_t)atoi(menv) * 1024);
     int stages[3] = {nenv ? std::max(1, std::min(3, atoi(nenv))) : 2, 2, 1};
+    if (getenv("HGM_SINGLE_STAGE"))  // testing: every budget single-staged (the large-T fallback path)
+        stages[0] = stages[1] = 1;
     if (T > 128 && !benv && !nenv) {
         // b-tiles are single frames here (FT_max = 1) and items are a-frame chunks whose
         // fixed part (b-row entries, row tables) is amortised over the chunk: one 220 KB
@@ -261,6 +268,10 @@ static bool window_path(const hgm_scene *sc, const std::vector<InstDesc> &all, i
         c.SW = std::max(c.SW, d.we - d.wb);
     }
     if (c.SW >= 32768) return false;  // tasks pack node indices in 15 / 16 bits
+    // a handful of LARGE windows: one CTA per window would leave the GPU idle where the
+    // per-step kernel spreads each step over every SM (one 754-node window, T = 10:
+    // 0.45 ms on K-DPW vs 0.26 ms fused)
+    if (!(e && strcmp(e, "window") == 0) && all.size() < 4 && c.NPP > 2048) return false;
     const size_t limit = 227 * 1024;
     if (dp_window_smem(c, NM) > limit) return false;  // even without a task list
     // tasks of the busiest window, bounded from the frame histogram: per b-frame fb,
@@ -289,7 +300,7 @@ static bool window_path(const hgm_scene *sc, const std::vector<InstDesc> &all, i
 // U: batched unary table U[((i * nn) + (n - n_lo)) * NM + k].
 hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *sc, const hgm_params &pp,
                        const hgm_offsets &o, const float *U, const float *Us, int64_t n_lo, int64_t nn,
-                       const MatchOut *outs, cudaStream_t s) {
+                       const MatchOut *outs, cudaStream_t s, int lane) {
     const int count = o.count, M = models[0]->M;
     if (count <= 0) return HGM_OK;
     if (NM < 1 || NM > MAX_BATCH) return fail(HGM_ERR_INVALID_ARGUMENT, "model batch size must be 1..8");
@@ -414,8 +425,9 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
     // (C4, ~8 windows per chunk: 21-32 % less time per call).  Many-window chunks (C3,
     // ~800 per 6 GiB chunk) are faster on one lane, and a second lane doubles the history.
     const char *senv = getenv("HGM_STREAMS");  // 1 / 2: force
-    const int nlanes = senv ? (atoi(senv) == 2 ? 2 : 1)
-                            : ((chunks.size() >= 3 && (int64_t)count < 64 * (int64_t)chunks.size()) ? 2 : 1);
+    const int nlanes = lane > 0 ? 1  // a concurrent model batch: its lane is the only one
+                                : senv ? (atoi(senv) == 2 ? 2 : 1)
+                                       : ((chunks.size() >= 3 && (int64_t)count < 64 * (int64_t)chunks.size()) ? 2 : 1);
     struct Lane {
         cudaStream_t s = nullptr;
         DevBuf hist, items, counters, book;
@@ -424,7 +436,7 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
     lanes[0].s = s;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     if (nlanes == 2) {
-        lanes[1].s = aux_stream(sc->device);
+        lanes[1].s = aux_stream(sc->device, 0);
         HGM_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
         HGM_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     }
@@ -439,7 +451,7 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
         HGM_CUDA(cudaEventRecord(ev_fork, s));
         HGM_CUDA(cudaStreamWaitEvent(lanes[1].s, ev_fork, 0));
     }
-    ScratchSet &scr = scratch_set(sc->device);
+    ScratchSet &scr = scratch_set(sc->device, lane);
     std::unique_lock<std::mutex> scr_lock(scr.mu);  // held while this call enqueues work on the buffers
     if (!scr.done) HGM_CUDA(cudaEventCreateWithFlags(&scr.done, cudaEventDisableTiming));
     HGM_CUDA(cudaStreamWaitEvent(s, scr.done, 0));  // the previous user's kernels are done with them

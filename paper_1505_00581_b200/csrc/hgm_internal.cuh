@@ -143,7 +143,11 @@ bool use_v0_kernels();
 extern thread_local bool g_tiling_failed;  // set by match_batch when a model batch must be split
 hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *sc, const hgm_params &pp,
                        const hgm_offsets &o, const float *U, const float *Us, int64_t n_lo, int64_t nn,
-                       const MatchOut *outs, cudaStream_t s);
+                       const MatchOut *outs, cudaStream_t s, int lane = 0);
+// lanes of concurrent model batches (detect): lane l > 0 runs on aux_stream(device, l)
+// with its own K-DP scratch set
+constexpr int MAX_LANES = 8;
+cudaStream_t aux_stream(int device, int idx);
 hgm_status offset_argmin(const float *score, int n_models, int count, float threshold, int32_t *winner,
                          float *best, cudaStream_t s);
 hgm_status chain_mean(const float *S_chain, const int32_t *chain_first, int n_models, int count, float *S_model,

@@ -39,7 +39,7 @@ def _worker(rank, world, port, clip, first, count, score_mode, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("count,score_mode,axis", [(300, 0, "offsets"), (4, 0, "models"), (2, 1, "models")])
+@pytest.mark.parametrize("count,score_mode,axis", [(300, 0, "offsets"), (3, 0, "models"), (1, 1, "models")])
 def test_two_ranks_on_gpu_equal_one_process(count, score_mode, axis):
     import torch
 
