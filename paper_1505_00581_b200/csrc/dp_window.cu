@@ -91,6 +91,17 @@ __device__ __forceinline__ int cta_excl_scan(int v, int *s_warp, int *total) {
     return r;
 }
 
+// Optional step trace (HGM_TRACE_W=1, diagnosis): globaltimer stamps of CTA 0 at the
+// phase boundaries of every step of one launch: [step][0..5]
+__device__ unsigned long long *g_wtrace = nullptr;
+__device__ __forceinline__ void wtrace(int s, int ev) {
+    if (g_wtrace && blockIdx.x == 0 && threadIdx.x == 0 && s < 256) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_wtrace[s * 6 + ev] = t;
+    }
+}
+
 template <int NM, int KW_THREADS>
 __global__ void __launch_bounds__(KW_THREADS) k_dp_window(SceneView sc, const InstDesc *__restrict__ inst,
                                                            float *__restrict__ hist, int64_t L, int M,
@@ -188,6 +199,7 @@ __global__ void __launch_bounds__(KW_THREADS) k_dp_window(SceneView sc, const In
     for (int s = 0; s < nsteps; ++s) {
         const int i = M - 1 - s;  // 0-based model node of this step; layer i - 2
         const bool has_next = s > 0;
+        wtrace(s, 0);
         // ---- step constants (model gaps / angles) and the Delta table
         if (tid == 0) {
             StepConstB kc{};
@@ -208,6 +220,7 @@ __global__ void __launch_bounds__(KW_THREADS) k_dp_window(SceneView sc, const In
         ++u_use;
         const float *Ui = UR + (((int64_t)i * nn + (wb - n_lo)) * NM & 3);
         __syncthreads();
+        wtrace(s, 1);
         // ---- phase 1: dummy-form terms per node, messages + (b, eps) minima per row
         for (int q = tid; q < Sw * NM; q += KW_THREADS) {
             const int c = q / NM, k = q - c * NM;
@@ -250,6 +263,7 @@ __global__ void __launch_bounds__(KW_THREADS) k_dp_window(SceneView sc, const In
         }
         if (tid == 0) bulk_wait_read_all();  // the previous layer's bulk store has read LAY
         __syncthreads();
+        wtrace(s, 2);
         if (tid == 0 && s + 1 < nsteps) issue_u(i - 1);  // UR is free: prefetch the next step's row
         // ---- phase 2a: dummy-form states of step i (cheap; every thread)
         for (int q = tid; q < Sw * NM; q += KW_THREADS) {
@@ -261,6 +275,7 @@ __global__ void __launch_bounds__(KW_THREADS) k_dp_window(SceneView sc, const In
         }
         if (tid < NM) LAY[EE * NM + tid] = EEN[tid];  // (eps, eps) of step i starts here ...
         __syncthreads();
+        wtrace(s, 3);
         for (int q = tid; q < Sw * NM; q += KW_THREADS) {
             const int k = q % NM;
             atomicMin(reinterpret_cast<unsigned *>(LAY + EE * NM + k), __float_as_uint(WC[q]));  // ... and is min-reduced (w >= 0)
@@ -324,8 +339,10 @@ __global__ void __launch_bounds__(KW_THREADS) k_dp_window(SceneView sc, const In
                 }
             }
         }
+        wtrace(s, 4);
         fence_async_smem();  // LAY's generic-proxy writes before the bulk store reads them
         __syncthreads();
+        wtrace(s, 5);
         if (tid == 0) {  // alpha_i -> the history (layer i - 2), one bulk store
             bulk_s2g(hist + (int64_t)(i - 2) * L + d.off, LAY, lay_bytes);
             bulk_commit();
@@ -353,7 +370,28 @@ static hgm_status launch_w(const SceneView &v, const InstDesc *dinst, int ninst,
             if (dev >= 0 && dev < 64) configured[d] = (int)smem;
         }
     }
+    static int traced = 0;
+    unsigned long long *tbuf = nullptr;
+    if (getenv("HGM_TRACE_W") && !traced) {  // diagnosis: per-step phase times of CTA 0, first launch
+        traced = 1;
+        cudaMalloc(&tbuf, 256 * 6 * 8);
+        cudaMemset(tbuf, 0, 256 * 6 * 8);
+        cudaMemcpyToSymbol(g_wtrace, &tbuf, sizeof(tbuf));
+    }
     k_dp_window<NM, NT><<<ninst, NT, smem, s>>>(v, dinst, hist, L, M, sp, U, nn, n_lo, p, caps);
+    if (tbuf) {
+        static unsigned long long h[256 * 6];
+        unsigned long long *z = nullptr;
+        cudaMemcpy(h, tbuf, sizeof(h), cudaMemcpyDeviceToHost);
+        cudaMemcpyToSymbol(g_wtrace, &z, sizeof(z));
+        cudaFree(tbuf);
+        fprintf(stderr, "HGM_TRACE_W NM %d threads %d windows %d smem %zu; per step (us): consts+U, phase1, 2a, 2b, store\n",
+                NM, NT, ninst, smem);
+        for (int st = 0; st < 256 && h[st * 6]; ++st)
+            fprintf(stderr, "step %3d %7.2f %7.2f %7.2f %7.2f %7.2f\n", st, (h[st * 6 + 1] - h[st * 6]) * 1e-3,
+                    (h[st * 6 + 2] - h[st * 6 + 1]) * 1e-3, (h[st * 6 + 3] - h[st * 6 + 2]) * 1e-3,
+                    (h[st * 6 + 4] - h[st * 6 + 3]) * 1e-3, (h[st * 6 + 5] - h[st * 6 + 4]) * 1e-3);
+    }
     return HGM_OK;
 }
 

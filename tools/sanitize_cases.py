@@ -43,12 +43,19 @@ def _c4_short(T, M, nf):
     return wl
 
 
+def _many_models():
+    wl = synth.make_workload("C2")
+    wl.models = wl.models * 3  # 18 models of equal M: batches of 8, 8, 2 on three lanes
+    return wl
+
+
 CASES = {
     "c0": lambda: [run(synth.make_workload("C0", seed=s)) for s in range(3)],
     "c1": lambda: run(synth.make_workload("C1"), count=120, ks=[0, 60, 119]),
     "c2": lambda: run(synth.make_workload("C2"), scene_idx=3, count=60, ks=[0, 30, 59]),
     "c4t80": lambda: run(_c4_short(80, 10, 420), models=[0, 1], ks=[0]),
     "single": lambda: run(synth.make_single(0, plant=True), ks=[0]),
+    "lanes": lambda: run(_many_models(), scene_idx=2, count=40, ks=[0, 39]),  # 3 concurrent model batches
 }
 
 if __name__ == "__main__":
