@@ -105,6 +105,7 @@ struct WinCaps {  // maxima over the windows of one launch
     int W;        // window length in frames
     int NTASK;    // task capacity (>= the tasks of every window)
     int T;
+    int M;        // chain length (the step constants of every step live in shared memory)
 };
 struct WinStepPtrs {
     const float4 *step[MAX_BATCH];  // per-model step constants (g_i, g_{i-1}, A1, K2), device

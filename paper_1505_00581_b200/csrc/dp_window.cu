@@ -39,7 +39,7 @@ namespace hgm {
 constexpr int KW_THREADS_MAX = 1024;
 
 struct WinPlan {  // shared-memory plan (byte offsets), sized by the launch's maxima
-    size_t th, ent, lay, ur, wc, bean, rmin, nt, nlo, nhi, nro, nfc, nlc, ftl, task, dl, kc, ctl, total;
+    size_t th, ent, lay, ur, wc, bean, rmin, nt, nlo, nhi, nro, nfc, nlc, ftl, task, dl, kc, kca, ctl, total;
     int lay_floats;
     __host__ __device__ WinPlan(const WinCaps &c, int NM) {
         size_t o = 0;
@@ -66,6 +66,7 @@ struct WinPlan {  // shared-memory plan (byte offsets), sized by the launch's ma
         task = take(4 * (size_t)c.NTASK);
         dl = take(4 * (size_t)c.T * NM);
         kc = take(sizeof(StepConstB));
+        kca = take(16 * (size_t)c.M * NM);   // step constants of every step (float4 per model)
         ctl = take(48 + 4 * (KW_THREADS_MAX / 32 + 1));
         total = o;
     }
@@ -98,7 +99,7 @@ __device__ __forceinline__ void wtrace(int s, int ev) {
     if (g_wtrace && blockIdx.x == 0 && threadIdx.x == 0 && s < 256) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        g_wtrace[s * 6 + ev] = t;
+        g_wtrace[s * 8 + ev] = t;
     }
 }
 
@@ -128,6 +129,7 @@ __global__ void __launch_bounds__(KW_THREADS) k_dp_window(SceneView sc, const In
     unsigned *TASK = reinterpret_cast<unsigned *>(smem + pl.task);
     float *DL = reinterpret_cast<float *>(smem + pl.dl);
     StepConstB *s_kc = reinterpret_cast<StepConstB *>(smem + pl.kc);
+    float4 *KCA = reinterpret_cast<float4 *>(smem + pl.kca);            // [M][NM] (g_i, g_{i-1}, A1, K2)
     uint64_t *ubar = reinterpret_cast<uint64_t *>(smem + pl.ctl);
     int *s_claim = reinterpret_cast<int *>(smem + pl.ctl + 8);
     int *s_ntask = reinterpret_cast<int *>(smem + pl.ctl + 12);
@@ -166,6 +168,7 @@ __global__ void __launch_bounds__(KW_THREADS) k_dp_window(SceneView sc, const In
     }
     for (int f = tid; f <= W; f += KW_THREADS) FTL[f] = min(max(sc.first(o + f), wb), d.we) - wb;
     for (int q = tid; q < npp; q += KW_THREADS) TH[q] = __ldg(sc.theta_pad + d.ppad + q);
+    for (int q = tid; q < M * NM; q += KW_THREADS) KCA[q] = __ldg(sp.step[q % NM] + q / NM);
     __syncthreads();
     // ---- task list (once): gap-major (longest candidate ranges first), per b-frame
     // segment (b, pair of a's of frame t'(b) - g): packed b | a0 << 16 | two << 31
@@ -203,7 +206,7 @@ __global__ void __launch_bounds__(KW_THREADS) k_dp_window(SceneView sc, const In
         // ---- step constants (model gaps / angles) and the Delta table
         if (tid == 0) {
             StepConstB kc{};
-            for (int k = 0; k < NM; ++k) kc.c[k] = __ldg(sp.step[k] + i);
+            for (int k = 0; k < NM; ++k) kc.c[k] = KCA[i * NM + k];
             for (int q = 0; q < (NM + 1) / 2; ++q) {
                 const int k1 = min(2 * q + 1, NM - 1);
                 kc.nA1[q] = make_float2(-kc.c[2 * q].z, -kc.c[k1].z);
@@ -214,7 +217,7 @@ __global__ void __launch_bounds__(KW_THREADS) k_dp_window(SceneView sc, const In
         }
         for (int q = tid; q < T * NM; q += KW_THREADS) {
             const int dt = q / NM, k = q - dt * NM;
-            DL[q] = delta_term(p.l2, __ldg(&sp.step[k][i].x), dt);
+            DL[q] = delta_term(p.l2, KCA[i * NM + k].x, dt);
         }
         mbar_wait(ubar, u_use & 1);  // U_i landed
         ++u_use;
@@ -228,6 +231,8 @@ __global__ void __launch_bounds__(KW_THREADS) k_dp_window(SceneView sc, const In
             BEAN[q] = __fadd_rn(p.l1W, has_next ? LAY[(npp + Sw + c) * NM + k] : 0.f);        // eps candidate
         }
         if (tid < NM) EEN[tid] = __fadd_rn(p.l1W, has_next ? LAY[EE * NM + tid] : 0.f);
+        // messages + (b, eps) minima, one warp per b row (measured faster than groups of
+        // 4-16 lanes per row on short rows: the per-group redux.sync masks serialise)
         for (int x = warp; x < Sw; x += KW_WARPS) {
             const int c0 = NLO[x], len = NHI[x] - c0, ro = NRO[x], tx = NT[x];
             float mn[NM];
@@ -261,7 +266,9 @@ __global__ void __launch_bounds__(KW_THREADS) k_dp_window(SceneView sc, const In
                 if (lane == k) RMIN[x * NM + k] = v;
             }
         }
+        wtrace(s, 6);
         if (tid == 0) bulk_wait_read_all();  // the previous layer's bulk store has read LAY
+        wtrace(s, 7);
         __syncthreads();
         wtrace(s, 2);
         if (tid == 0 && s + 1 < nsteps) issue_u(i - 1);  // UR is free: prefetch the next step's row
@@ -281,15 +288,22 @@ __global__ void __launch_bounds__(KW_THREADS) k_dp_window(SceneView sc, const In
             atomicMin(reinterpret_cast<unsigned *>(LAY + EE * NM + k), __float_as_uint(WC[q]));  // ... and is min-reduced (w >= 0)
         }
         // ---- phase 2b: real states, 32-task groups claimed by warps
+        // Few tasks for the CTA's threads (small windows): LPT = 2 or 4 lanes share a task, each
+        // taking a contiguous share of its candidates, and the shares' minima are combined by
+        // shuffles -- min is exact and order-free, so the result is the same bits, while the
+        // step's critical path (the longest task) shrinks by LPT.
         const StepConstB kc = *s_kc;
         const int ntask = *s_ntask;
+        const int lsh = ntask * 4 <= KW_THREADS ? 2 : (ntask * 2 <= KW_THREADS ? 1 : 0);
+        const int LPT = 1 << lsh, sub = lane & (LPT - 1);
         for (;;) {
             int t0 = 0;
-            if (lane == 0) t0 = atomicAdd(s_claim, 32);
+            if (lane == 0) t0 = atomicAdd(s_claim, 32 >> lsh);
             t0 = __shfl_sync(0xffffffffu, t0, 0);
             if (t0 >= ntask) break;
-            const bool live = t0 + lane < ntask;
-            const unsigned tk = TASK[live ? t0 + lane : ntask - 1];
+            const int ti = t0 + (lane >> lsh);
+            const bool live = ti < ntask;
+            const unsigned tk = TASK[live ? ti : ntask - 1];
             const int b = (int)(tk & 0xffffu), a0 = (int)((tk >> 16) & 0x7fffu);
             const bool two = live && (tk >> 31);
             const int a1 = two ? a0 + 1 : a0;
@@ -308,12 +322,15 @@ __global__ void __launch_bounds__(KW_THREADS) k_dp_window(SceneView sc, const In
             float R0[NM], R1[NM];
 #pragma unroll
             for (int k = 0; k < NM; ++k) R0[k] = R1[k] = INFINITY;
+            const int per = (trip + LPT - 1) >> lsh;  // this lane's share [jb, je) of the candidates
+            const int jb = min(trip, sub * per), je = min(trip, jb + per);
             if (!__any_sync(0xffffffffu, dirty)) {
-                task_loop<NM, EPF>(erow, arow0, arow1, th_ab0, th_ab1, trip, kc, p.l23, R0, R1);
+                task_loop<NM, EPF>(erow + (size_t)jb * EPF, arow0 + jb, arow1 + jb, th_ab0, th_ab1, je - jb, kc, p.l23,
+                                   R0, R1);
             } else {  // exact flag-aware loop (coincident points, R10): NaN directions mark them
                 const bool co_ab0 = live && isnan(th_ab0);
                 const bool co_ab1 = live && isnan(th_ab1);
-                for (int j = 0; j < trip; ++j) {
+                for (int j = jb; j < je; ++j) {
                     float e0[EPF];
                     ld_went<EPF>(erow + (size_t)j * EPF, e0);
                     const bool cbc = isnan(e0[NM]);
@@ -328,7 +345,14 @@ __global__ void __launch_bounds__(KW_THREADS) k_dp_window(SceneView sc, const In
                     }
                 }
             }
-            if (live) {
+            for (int o = 1; o < LPT; o <<= 1) {  // combine the shares (lanes of a task are adjacent)
+#pragma unroll
+                for (int k = 0; k < NM; ++k) {
+                    R0[k] = fminf(R0[k], __shfl_xor_sync(0xffffffffu, R0[k], o));
+                    R1[k] = fminf(R1[k], __shfl_xor_sync(0xffffffffu, R1[k], o));
+                }
+            }
+            if (live && sub == 0) {
                 const int g = NT[b] - NT[a0];
 #pragma unroll
                 for (int k = 0; k < NM; ++k) {
@@ -374,23 +398,25 @@ static hgm_status launch_w(const SceneView &v, const InstDesc *dinst, int ninst,
     unsigned long long *tbuf = nullptr;
     if (getenv("HGM_TRACE_W") && !traced) {  // diagnosis: per-step phase times of CTA 0, first launch
         traced = 1;
-        cudaMalloc(&tbuf, 256 * 6 * 8);
-        cudaMemset(tbuf, 0, 256 * 6 * 8);
+        cudaMalloc(&tbuf, 256 * 8 * 8);
+        cudaMemset(tbuf, 0, 256 * 8 * 8);
         cudaMemcpyToSymbol(g_wtrace, &tbuf, sizeof(tbuf));
     }
     k_dp_window<NM, NT><<<ninst, NT, smem, s>>>(v, dinst, hist, L, M, sp, U, nn, n_lo, p, caps);
     if (tbuf) {
-        static unsigned long long h[256 * 6];
+        static unsigned long long h[256 * 8];
         unsigned long long *z = nullptr;
         cudaMemcpy(h, tbuf, sizeof(h), cudaMemcpyDeviceToHost);
         cudaMemcpyToSymbol(g_wtrace, &z, sizeof(z));
         cudaFree(tbuf);
-        fprintf(stderr, "HGM_TRACE_W NM %d threads %d windows %d smem %zu; per step (us): consts+U, phase1, 2a, 2b, store\n",
-                NM, NT, ninst, smem);
-        for (int st = 0; st < 256 && h[st * 6]; ++st)
-            fprintf(stderr, "step %3d %7.2f %7.2f %7.2f %7.2f %7.2f\n", st, (h[st * 6 + 1] - h[st * 6]) * 1e-3,
-                    (h[st * 6 + 2] - h[st * 6 + 1]) * 1e-3, (h[st * 6 + 3] - h[st * 6 + 2]) * 1e-3,
-                    (h[st * 6 + 4] - h[st * 6 + 3]) * 1e-3, (h[st * 6 + 5] - h[st * 6 + 4]) * 1e-3);
+        fprintf(stderr, "HGM_TRACE_W NM %d threads %d windows %d smem %zu; per step (us, thread 0): consts+U, "
+                "phase1 (own rows), bulk-store read wait, sync, 2a, 2b, sync\n", NM, NT, ninst, smem);
+        for (int st = 0; st < 256 && h[st * 8]; ++st) {
+            const unsigned long long *q = h + st * 8;
+            fprintf(stderr, "step %3d %7.2f %7.2f %7.2f %7.2f %7.2f %7.2f %7.2f\n", st, (q[1] - q[0]) * 1e-3,
+                    (q[6] - q[1]) * 1e-3, (q[7] - q[6]) * 1e-3, (q[2] - q[7]) * 1e-3, (q[3] - q[2]) * 1e-3,
+                    (q[4] - q[3]) * 1e-3, (q[5] - q[4]) * 1e-3);
+        }
     }
     return HGM_OK;
 }
@@ -410,11 +436,12 @@ static hgm_status launch_nm_w(const SceneView &v, const InstDesc *dinst, int nin
     const int k = ninst < nsm ? 1 : std::min(per_sm, (ninst + nsm - 1) / nsm);
     int nt = k <= 1 ? 1024 : (k == 2 ? 512 : 256);
     if (const char *e = getenv("HGM_WIN_THREADS")) nt = atoi(e);  // tuning knob
+    const WinCaps &c = caps;
     if constexpr (NM <= 2) {
-        if (nt >= 1024) return launch_w<NM, 1024>(v, dinst, ninst, hist, L, M, sp, U, nn, n_lo, p, caps, s);
+        if (nt >= 1024) return launch_w<NM, 1024>(v, dinst, ninst, hist, L, M, sp, U, nn, n_lo, p, c, s);
     }
-    if (nt >= 512) return launch_w<NM, 512>(v, dinst, ninst, hist, L, M, sp, U, nn, n_lo, p, caps, s);
-    return launch_w<NM, 256>(v, dinst, ninst, hist, L, M, sp, U, nn, n_lo, p, caps, s);
+    if (nt >= 512) return launch_w<NM, 512>(v, dinst, ninst, hist, L, M, sp, U, nn, n_lo, p, c, s);
+    return launch_w<NM, 256>(v, dinst, ninst, hist, L, M, sp, U, nn, n_lo, p, c, s);
 }
 
 hgm_status launch_dp_window(int NM, const SceneView &v, const InstDesc *dinst, int ninst, float *hist, int64_t L,

@@ -259,10 +259,10 @@ static bool make_tiling(const hgm_scene *sc, const hgm_offsets &o, int T, int NM
 // histogram (one task = a b with a pair of a's of one frame).  HGM_DP=fused / window
 // forces a path (the window path still needs to fit).
 static bool window_path(const hgm_scene *sc, const std::vector<InstDesc> &all, int NM, const hgm_offsets &o, int T,
-                        WinCaps *caps) {
+                        int M, WinCaps *caps) {
     const char *e = getenv("HGM_DP");
     if (e && strcmp(e, "fused") == 0) return false;
-    WinCaps c{0, 0, o.window, 0, T};
+    WinCaps c{0, 0, o.window, 0, T, M};
     for (const InstDesc &d : all) {
         c.NPP = std::max(c.NPP, d.npp);
         c.SW = std::max(c.SW, d.we - d.wb);
@@ -323,7 +323,7 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
         all[k] = d;
     }
     WinCaps wcaps{};
-    const bool win = !v0 && nsteps > 0 && window_path(sc, all, NM, o, pp.T, &wcaps);
+    const bool win = !v0 && nsteps > 0 && window_path(sc, all, NM, o, pp.T, M, &wcaps);
     if (win && getenv("HGM_DEBUG_TILING"))
         fprintf(stderr, "window kernel: NM %d NPP %d SW %d NTASK %d smem %zu windows %d\n", NM, wcaps.NPP, wcaps.SW,
                 wcaps.NTASK, dp_window_smem(wcaps, NM), count);

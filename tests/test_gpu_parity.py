@@ -353,7 +353,8 @@ def test_dense_fallbacks_bitexact(hgm, monkeypatch):
 @pytest.mark.parametrize("smem_kb", [20, 32, 48, 110])
 def test_tile_sizes_bitexact(hgm, smem_kb, monkeypatch):
     """Shared-memory budgets from tiny (one-frame tiles whose a-frames are split into
-    chunks, single-stage items) to the default: every tiling gives the v0 bits."""
+    chunks, single-stage items) to the default: every tiling of the per-step kernel
+    (HGM_DP=fused; C1 itself runs on the per-window kernel by default) gives the v0 bits."""
     import torch
 
     wl = synth.make_workload("C1")
@@ -363,6 +364,7 @@ def test_tile_sizes_bitexact(hgm, smem_kb, monkeypatch):
     monkeypatch.setenv("HGM_KERNEL", "v0")
     a = hgm.match_model_at_offsets(m, s, p, 0, 1, 541, 60)
     monkeypatch.setenv("HGM_KERNEL", "v1")
+    monkeypatch.setenv("HGM_DP", "fused")
     monkeypatch.setenv("HGM_SMEM_KB", str(smem_kb))
     b = hgm.match_model_at_offsets(m, s, p, 0, 1, 541, 60)
     torch.cuda.synchronize()

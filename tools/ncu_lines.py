@@ -15,7 +15,11 @@ acc = defaultdict(lambda: [0.0, 0.0])
 src = {}
 hdr = None
 line = None
+fname = "?"
 for r in rows:
+    if r and r[0] == "File Name":
+        fname = r[1].rsplit("/", 1)[-1]
+        continue
     if r and r[0] == "Line No":
         hdr = r
         idx = {n: i for i, n in enumerate(r)}
@@ -25,7 +29,7 @@ for r in rows:
     if not hdr or len(r) < len(hdr):
         continue
     if r[0]:
-        line = int(r[0])
+        line = (fname, int(r[0]))
         src[line] = r[1]
     if line is not None and r[2]:
         def f(x):
@@ -38,4 +42,4 @@ for r in rows:
 te = sum(v[0] for v in acc.values()) or 1
 ts = sum(v[1] for v in acc.values()) or 1
 for ln, (e, s) in sorted(acc.items(), key=lambda kv: -kv[1][0])[:top]:
-    print(f"{ln:5d} {100 * e / te:5.1f}% inst {100 * s / ts:5.1f}% samp | {src.get(ln, '').strip()[:90]}")
+    print(f"{ln[0][:16]:16s}{ln[1]:5d} {100 * e / te:5.1f}% inst {100 * s / ts:5.1f}% samp | {src.get(ln, '').strip()[:90]}")
