@@ -413,13 +413,22 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
         mbar_wait(&ctl->conv[s], use & 1);  // all rows of the item are messages now
         // ---- P3: real states.  A lane task is one b with a PAIR of a's of the same a-frame
         // (same candidate range), so each candidate entry (b, c_j) is loaded once for two
-        // states; warps claim 32-task groups (segments by descending trip count).
+        // states; warps claim 32-task groups (segments by descending trip count).  An item
+        // with few tasks and long trips (large T: a few hundred states of hundreds of
+        // candidates) would leave warps idle behind the one holding the last group, so there
+        // LPT = 2..8 lanes share a task, each taking a contiguous share of its candidates, and
+        // the shares' minima are combined by shuffles (min is exact and order-free: same bits).
+        int lsh = 0;  // (a cost model that also split mid-size items measured 11-16 % slower on C4
+                      // T = 40 / rho = 8: each share repeats the task decode and the combine)
+        if (nst > 0)  // seg[0]: the longest trip (descending order); shares of >= 48 candidates
+            while (lsh < 3 && (nst << (lsh + 1)) <= 8 * KDP_THREADS && (seg[0].trip >> (lsh + 1)) >= 48) ++lsh;
+        const int LPT = 1 << lsh, sub = lane & (LPT - 1);
         for (;;) {
             int s0 = 0;
-            if (lane == 0) s0 = atomicAdd(&ctl->task_claim[s], 32);
+            if (lane == 0) s0 = atomicAdd(&ctl->task_claim[s], 32 >> lsh);
             s0 = __shfl_sync(0xffffffffu, s0, 0);
             if (s0 >= nst) break;
-            const int st = s0 + lane;
+            const int st = s0 + (lane >> lsh);
             const bool live = st < nst;
             const Seg sg = seg[live ? smap[st] : smap[nst - 1]];
             int trip = 0, b = B0, a0 = A0;
@@ -446,13 +455,16 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
             float R0[NM], R1[NM];
 #pragma unroll
             for (int k = 0; k < NM; ++k) R0[k] = R1[k] = INFINITY;
+            const int per = (trip + LPT - 1) >> lsh;  // this lane's share [jb, je) of the candidates
+            const int jb = min(trip, sub * per), je = min(trip, jb + per);
             if (!__any_sync(0xffffffffu, dirty)) {
-                task_loop<NM, EPF>(erow, arow0, arow1, th_ab0, th_ab1, trip, kc, p.l23, R0, R1);
+                task_loop<NM, EPF>(erow + (size_t)jb * EPF, arow0 + jb, arow1 + jb, th_ab0, th_ab1, je - jb, kc, p.l23,
+                                   R0, R1);
             } else {  // exact flag-aware loop (coincident points, R10): the padded band holds NaN
                       // for the direction of a zero-length ray, so the flags come with the angles
                 const bool co_ab0 = live && isnan(th_ab0);
                 const bool co_ab1 = live && isnan(th_ab1);
-                for (int j = 0; j < trip; ++j) {
+                for (int j = jb; j < je; ++j) {
                     float e0[EPF];
                     ld_entry<EPF>(erow + (size_t)j * EPF, e0);
                     const bool cbc = isnan(e0[NM]);
@@ -467,7 +479,14 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
                     }
                 }
             }
-            if (live) {
+            for (int o = 1; o < LPT; o <<= 1) {  // combine the shares (the lanes of a task are adjacent)
+#pragma unroll
+                for (int k = 0; k < NM; ++k) {
+                    R0[k] = fminf(R0[k], __shfl_xor_sync(0xffffffffu, R0[k], o));
+                    R1[k] = fminf(R1[k], __shfl_xor_sync(0xffffffffu, R1[k], o));
+                }
+            }
+            if (live && sub == 0) {
                 float out0[EPF], out1[EPF];
 #pragma unroll
                 for (int k = 0; k < NM; ++k) {
