@@ -187,3 +187,24 @@ def test_sharded_detect_equals_single_process_gloo():
         w, s = out[r]
         assert w == ref.winner.tolist()
         assert np.array_equal(np.array(s, np.float32), ref.score.astype(np.float32))
+
+
+def test_bench_gpus_flag_spawns_ranks():
+    """`python bench.py --gpus 2` without a launcher re-executes itself under
+    torch.distributed.run (127.0.0.1): exactly one JSON line (rank 0) with n_gpus = 2.
+    Exercised through the reference arm, which runs on the host cores (no GPU here)."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "2",
+                          "--steps", "1", "--warmup", "0", "--cpu-seconds", "1", "--frames-per-gpu", "800"],
+                         capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference" and d["value"] > 0
+    assert "spawning 2 ranks" in out.stderr
