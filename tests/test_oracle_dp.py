@@ -242,3 +242,30 @@ def test_appearance_distance_C0_independent(seed):
         E, Er, A, z = oracle.match(model, scene, pp)
         u = [wd if z[i] < 0 else float(np.linalg.norm(model.f[i] - scene.f[z[i]])) for i in range(model.n)]
         assert A == pytest.approx(sum(u), rel=1e-12, abs=1e-12), (seed, wd)
+
+
+def test_same_frame_pair_is_not_admissible_reading_R1():
+    """Reading R1: consecutive real labels lie in strictly
+    later scene frames (Eq. 7's biconditional; 'lower'; ]z - T, z[,
+    P:L312).  SPEC D-2's example (zPrev and zPrevPrev both in frame 5, increasing node index
+    -> admissible) is deliberately NOT followed.  Pinned on the smallest case that
+    tells the two readings apart: a 2-node model (frames 0, 1) against two scene nodes that
+    copy its descriptors exactly but share frame 5.  Under D-2 both could be matched (E* = 0);
+    under R1 at most one is real, so E* = lambda1 W^d (one exact match + one dummy), and the
+    brute force (declarative predicate) agrees."""
+    F = 3
+    f = np.array([[1.0, 0.0, 0.0], [0.0, 1.0, 0.0]])
+    model = oracle.NodeSet(np.array([0, 1], np.int32), np.array([10.0, 20.0]), np.array([10.0, 10.0]), f)
+    scene = oracle.NodeSet(np.array([5, 5], np.int32), np.array([10.0, 20.0]), np.array([10.0, 10.0]), f.copy())
+    p = dict(lambda1=0.6, lambda2=0.2, lambda3=5.0, w_dummy=0.5, T=10)
+    E, Er, A, z = oracle.match(model, scene, p)
+    assert E == pytest.approx(p["lambda1"] * p["w_dummy"], rel=1e-15)
+    assert sorted(int(v) for v in z).count(-1) == 1  # exactly one dummy
+    assert not oracle.feasible(model, scene, p, [0, 1])  # the declarative predicate (brute force's)
+    Eb, zb, _ = oracle.brute(model, scene, p)
+    assert Eb == pytest.approx(E, rel=1e-12) and list(zb) == list(z)
+    # one frame apart, the same two nodes are admissible and match exactly
+    scene2 = oracle.NodeSet(np.array([5, 6], np.int32), scene.x, scene.y, f.copy())
+    E2, _, _, z2 = oracle.match(model, scene2, p)
+    assert E2 == 0.0 and list(z2) == [0, 1]
+    assert F == f.shape[1]
