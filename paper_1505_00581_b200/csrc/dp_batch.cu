@@ -204,8 +204,11 @@ __device__ __forceinline__ void issue_stage(const SceneView &sc, WorkItem &w, co
     cl.close();  // (the stage was released by the consumers' empty[s] arrivals, after their reads)
 }
 
-template <int NM, bool kHasNext>
-__global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const WorkItem *__restrict__ items,
+#ifndef HGM_KDP_MINB
+#define HGM_KDP_MINB 2  // CTAs per SM the register allocation must allow (3 measured 11 % slower on C3)
+#endif
+template <int NM, bool kHasNext, bool kSplit>
+__global__ void __launch_bounds__(KDP_BLOCK, HGM_KDP_MINB) k_dp_fused(SceneView sc, const WorkItem *__restrict__ items,
                                                              int nitems, int *__restrict__ counter,
                                                              float *__restrict__ hist, int64_t L, int layer,
                                                              int has_prev, StepConstB kc, const float *__restrict__ U,
@@ -420,8 +423,10 @@ __global__ void __launch_bounds__(KDP_BLOCK, 2) k_dp_fused(SceneView sc, const W
         // the shares' minima are combined by shuffles (min is exact and order-free: same bits).
         int lsh = 0;  // (a cost model that also split mid-size items measured 11-16 % slower on C4
                       // T = 40 / rho = 8: each share repeats the task decode and the combine)
-        if (nst > 0)  // seg[0]: the longest trip (descending order); shares of >= 48 candidates
-            while (lsh < 3 && (nst << (lsh + 1)) <= 8 * KDP_THREADS && (seg[0].trip >> (lsh + 1)) >= 48) ++lsh;
+        if constexpr (kSplit) {  // (a launch-time choice: compiled in, the split costs C3 1.9 %)
+            if (nst > 0)  // seg[0]: the longest trip (descending order); shares of >= 48 candidates
+                while (lsh < 3 && (nst << (lsh + 1)) <= 8 * KDP_THREADS && (seg[0].trip >> (lsh + 1)) >= 48) ++lsh;
+        }
         const int LPT = 1 << lsh, sub = lane & (LPT - 1);
         for (;;) {
             int s0 = 0;
@@ -688,17 +693,20 @@ static hgm_status launch_nm(const SceneView &v, const WorkItem *items, int nitem
                             const StepConstB &kc, const float *U, int64_t ui_off, const DPParams &p,
                             const TileCaps &caps, cudaStream_t s) {
     const size_t smem = dp_batch_smem(caps, p.T, NM);
-    auto kern = has_next ? k_dp_fused<NM, true> : k_dp_fused<NM, false>;
+    // task splitting (kSplit) only where trips can be long enough to split (T >= 40)
+    const bool split = p.T >= 40;
+    auto kern = split ? (has_next ? k_dp_fused<NM, true, true> : k_dp_fused<NM, false, true>)
+                      : (has_next ? k_dp_fused<NM, true, false> : k_dp_fused<NM, false, false>);
     int dev = 0;
     HGM_CUDA(cudaGetDevice(&dev));
     // the shared-memory attribute applies per device context: cache it per device (and the
     // occupancy it gives), under a lock -- calls on different devices / threads may race here
     static std::mutex mu;
-    static int configured[64][2], occ[64][2], nsm_of[64];
+    static int configured[64][4], occ[64][4], nsm_of[64];
     int bps = 1, nsm = 0;
     {
         std::lock_guard<std::mutex> lk(mu);
-        const int d = dev < 0 || dev >= 64 ? 0 : dev, h = has_next ? 1 : 0;
+        const int d = dev < 0 || dev >= 64 ? 0 : dev, h = (has_next ? 1 : 0) + (split ? 2 : 0);
         if (dev < 0 || dev >= 64 || (int)smem > configured[d][h] || !nsm_of[d]) {
             HGM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             int b = 0;
