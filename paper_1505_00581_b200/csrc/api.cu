@@ -66,7 +66,14 @@ cudaEvent_t take_event() {  // g_mu held
 
 bool profiling() { return g_prof; }
 
+// NVTX ranges (SURVEY.md §5 tracing): every phase timer also opens a host range named after
+// its kernel class, so an nsys / ncu --nvtx timeline shows the scene build, unary table,
+// recursion, backtrack and argmin of each call; NVTX3 is header-only and its calls are
+// no-ops unless a tool is attached.
+static const char *const kPhaseName[] = {"hgm:scene (K-G)", "hgm:model", "hgm:unary (K-U)", "hgm:recursion (K-DP)",
+                                         "hgm:backtrack (K-BT)", "hgm:argmin (K-ARG)", "hgm:messages"};
 Timer::Timer(cudaStream_t s_, int cls_) : s(s_), cls(cls_) {
+    nvtxRangePushA(kPhaseName[cls_ >= 0 && cls_ <= K_MSG ? cls_ : 0]);
     if (!g_prof) return;
     {
         std::lock_guard<std::mutex> lk(g_mu);
@@ -76,6 +83,7 @@ Timer::Timer(cudaStream_t s_, int cls_) : s(s_), cls(cls_) {
     cudaEventRecord(a, s);
 }
 Timer::~Timer() {
+    nvtxRangePop();
     if (!a) return;
     cudaEventRecord(b, s);
     std::lock_guard<std::mutex> lk(g_mu);
@@ -274,6 +282,7 @@ const char *hgm_last_error(void) { return g_err.c_str(); }
 const char *hgm_version(void) { return "hgm 0.1 (sm_100a)"; }
 
 hgm_status hgm_build_model_graph(const hgm_points *pts, int device, hgm_model **out) {
+    NvtxRange nvtx_("hgm_build_model_graph");
     HGM_TRY(check_points(pts));
     if (!out) return fail(HGM_ERR_INVALID_ARGUMENT, "out == NULL");
     HGM_CUDA(cudaSetDevice(device));
@@ -298,6 +307,7 @@ hgm_status hgm_build_model_graph_dev(const hgm_points *pts, void *stream, hgm_mo
 }
 
 hgm_status hgm_build_model_chain(const hgm_points *pts, int device, int32_t rank, hgm_model **out) {
+    NvtxRange nvtx_("hgm_build_model_chain");
     HGM_TRY(check_points(pts));
     if (!out) return fail(HGM_ERR_INVALID_ARGUMENT, "out == NULL");
     if (rank < 0) return fail(HGM_ERR_INVALID_ARGUMENT, "rank < 0");
@@ -328,6 +338,7 @@ void hgm_free_model(hgm_model *m) {
 }
 
 hgm_status hgm_build_scene_index(const hgm_points *pts, int device, int32_t T_max, hgm_scene **out) {
+    NvtxRange nvtx_("hgm_build_scene_index");
     HGM_TRY(check_points(pts));
     if (!out) return fail(HGM_ERR_INVALID_ARGUMENT, "out == NULL");
     if (T_max < 1) return fail(HGM_ERR_INVALID_ARGUMENT, "T_max < 1");
@@ -377,6 +388,7 @@ static void covered_range(const hgm_scene *sc, const hgm_offsets *o, int64_t *lo
 
 hgm_status hgm_match_model_at_offsets(const hgm_model *model, const hgm_scene *scene, const hgm_params *params,
                                       const hgm_offsets *offsets, float *E, float *A, int64_t *z, void *stream) {
+    NvtxRange nvtx_("hgm_match_model_at_offsets");
     if (!model || !scene) return fail(HGM_ERR_INVALID_ARGUMENT, "NULL handle");
     HGM_TRY(check_params(params, scene));
     HGM_TRY(check_offsets(offsets));
@@ -547,6 +559,7 @@ static hgm_status finish_detect(const float *S, int n_models, int count, float t
 hgm_status hgm_detect_actions(const hgm_model *const *models, int32_t n_models, const hgm_scene *scene,
                               const hgm_params *params, const hgm_offsets *offsets, int32_t score_mode,
                               float threshold, int32_t *winner, float *score, float *E_all, void *stream) {
+    NvtxRange nvtx_("hgm_detect_actions");
     HGM_TRY(check_dictionary(models, n_models, scene, params, offsets, score_mode));
     const int count = offsets->count;
     if (count == 0) return HGM_OK;
@@ -571,6 +584,7 @@ hgm_status hgm_detect_chains(const hgm_model *const *chains, int32_t n_chains, c
                              int32_t n_models, const hgm_scene *scene, const hgm_params *params,
                              const hgm_offsets *offsets, int32_t score_mode, float threshold, int32_t *winner,
                              float *score, float *S_all, void *stream) {
+    NvtxRange nvtx_("hgm_detect_chains");
     HGM_TRY(check_dictionary(chains, n_chains, scene, params, offsets, score_mode));
     if (!chain_model) return fail(HGM_ERR_INVALID_ARGUMENT, "chain_model == NULL");
     if (n_models < 1) return fail(HGM_ERR_EMPTY_POINT_SET, "no models");
@@ -608,6 +622,7 @@ hgm_status hgm_classify_blocks(const hgm_model *const *prototypes, int32_t n_pro
                                int32_t n_labels, const hgm_scene *scene, const hgm_params *params,
                                const hgm_offsets *blocks, float threshold, int32_t *block_label, float *block_score,
                                int32_t *clip_label, void *stream) {
+    NvtxRange nvtx_("hgm_classify_blocks");
     if (!prototypes || !scene || !params || !blocks) return fail(HGM_ERR_INVALID_ARGUMENT, "NULL argument");
     if (n_prototypes < 1) return fail(HGM_ERR_EMPTY_POINT_SET, "empty prototype dictionary");
     if (!label) return fail(HGM_ERR_INVALID_ARGUMENT, "label == NULL");

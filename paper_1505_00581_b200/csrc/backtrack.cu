@@ -163,54 +163,57 @@ __global__ void __launch_bounds__(256) k_backtrack(SceneView sc, const InstDesc 
     auto a_be = [&](const float *l, int b) { return at(l, d.ntail + (b - d.wb)); };
     auto a_ea = [&](const float *l, int a) { return at(l, d.ntail + Sw + (a - d.wb)); };
     auto a_ee = [&](const float *l) { return at(l, d.ntail + 2 * Sw); };
+    // The backtrack is a chain of M - 2 dependent steps, so its time is the latency of
+    // each step's dependent loads.  Per node one int4 (t', minnode(t'+1), qstart, qpad)
+    // replaces separate t / first / qstart / qpad loads and is carried from step to step
+    // (z_{i-2} <- z_{i-1} <- z_i); the next step's direction theta(z_{i-1} -> z_i), its
+    // candidate-range end and z_i's node info are issued together as soon as z_i is known;
+    // the padded band's NaN marks coincident pairs (the flags ride on the angles, as in
+    // K-DP); the appearance term of z_i is added one step late so its load never stalls
+    // the chain (the sum keeps its order i = 0, 1, ..., M-1).
+    const int4 NOI = make_int4(0, 0, 0, 0);
     int za = bst.z1, zb = bst.z2;  // z1, z2 (EPSL = dummy)
     int64_t *zo = bt.z[kk] ? bt.z[kk] + (int64_t)d.out * M : nullptr;
     float A = za == EPSL ? p.W : U(0, za);
     if (lane == 0 && zo) zo[0] = za == EPSL ? -1 : sc.id[za];
+    float u_pend = 0.f;  // U(i-1, z_{i-1}), added at step i
     if (M >= 2) {
-        A = __fadd_rn(A, zb == EPSL ? p.W : U(1, zb));
+        u_pend = zb == EPSL ? p.W : U(1, zb);
         if (lane == 0 && zo) zo[1] = zb == EPSL ? -1 : sc.id[zb];
     }
-    // ---- Eq. 12 backtrack, beta_i re-evaluated with the DP's arithmetic
+    int4 na = za != EPSL ? __ldg(sc.ninfo + za) : NOI, nb = zb != EPSL ? __ldg(sc.ninfo + zb) : NOI;
+    // theta(a -> b) (padded band, NaN = coincident) and the candidate-range end of the state
+    float th_ab = (za != EPSL && zb != EPSL) ? __ldg(sc.theta_pad + na.w + (zb - na.y)) : 0.f;
+    int hi_a = za != EPSL ? sc.first(na.x + T) : 0;
     for (int i = 2; i < M; ++i) {
         const float *nx = layer(i + 1);
         const float4 kc = bt.step[kk][i];
-        int c0, c1;
         const bool rb = zb != EPSL, ra = za != EPSL;
+        int c0, c1;
         if (rb) {
-            c0 = sc.first(sc.t[zb] + 1);
-            c1 = min(sc.first((ra ? sc.t[za] : sc.t[zb]) + T), d.we);
+            c0 = nb.y;
+            c1 = min(ra ? hi_a : sc.first(nb.x + T), d.we);
         } else if (ra) {
-            c0 = sc.first(sc.t[za] + 1);
-            c1 = min(sc.first(sc.t[za] + T), d.we);
+            c0 = na.y;
+            c1 = min(hi_a, d.we);
         } else {
             c0 = d.wb;
             c1 = d.we;
         }
-        float th_ab = 0.f;
-        bool co_ab = false;
-        int qa = 0, qb = 0, qbp = 0, aoff = 0, tb = 0;
-        if (rb && ra) {
-            qa = sc.qstart[za];
-            const int loa = sc.first(sc.t[za] + 1);
-            th_ab = sc.theta[qa + (zb - loa)];
-            co_ab = sc.coinc[qa + (zb - loa)];
-            aoff = c0 - loa;
-        }
-        if (rb) {
-            qb = sc.qstart[zb];
-            qbp = sc.qpad[zb] - d.ppad;
-            tb = sc.t[zb];
-        }
+        const bool co_ab = rb && ra && isnan(th_ab);
+        const int aoff = ra ? c0 - na.y : 0;
+        const int qbp = nb.w - d.ppad, tb = nb.x;
+        // the dummy candidate's value does not depend on the real ones: its load goes first
+        const float eps_nx = rb ? a_ea(nx, zb) : a_ee(nx);  // alpha_{i+1}(eps, b) or (eps, eps)
         auto value = [&](int c) -> float {
             const int j = c - c0;
             if (rb) {
                 const float n = msg_n(at(nx, qbp + j), Us(i, c));
                 if (!ra) return n;
-                const float m = msg_m(n, p.l2, kc.x, sc.t[c] - tb);
-                const bool cbc = sc.coinc[qb + j];
-                return cand_value(m, sc.theta[qb + j], th_ab, sc.theta[qa + aoff + j], cbc || co_ab,
-                                  cbc || sc.coinc[qa + aoff + j], kc.z, kc.w, p.l23);
+                const float m = msg_m(n, p.l2, kc.x, __ldg(sc.t + c) - tb);
+                const float th_bc = __ldg(sc.theta_pad + nb.w + j), th_ac = __ldg(sc.theta_pad + na.w + aoff + j);
+                const bool cbc = isnan(th_bc);
+                return cand_value(m, th_bc, th_ab, th_ac, cbc || co_ab, cbc || isnan(th_ac), kc.z, kc.w, p.l23);
             }
             return msg_n(a_be(nx, c), Us(i, c));
         };
@@ -242,22 +245,26 @@ __global__ void __launch_bounds__(256) k_backtrack(SceneView sc, const InstDesc 
                 arg = (int)__reduce_min_sync(0xffffffffu, lv == cm ? (unsigned)lc : 0xffffffffu);
             }
         }
-        float eps;
         float real = R;
-        if (rb && ra) {
-            real = __fadd_rn(R, state_const(p.l2, kc.y, tb - sc.t[za]));
-            eps = __fadd_rn(p.l1W, a_ea(nx, zb));
-        } else if (rb) {
-            eps = __fadd_rn(p.l1W, a_ea(nx, zb));
-        } else {
-            eps = __fadd_rn(p.l1W, a_ee(nx));
-        }
+        if (rb && ra) real = __fadd_rn(R, state_const(p.l2, kc.y, tb - na.x));
+        const float eps = __fadd_rn(p.l1W, eps_nx);
         const int zc = (arg >= 0 && real <= eps) ? arg : EPSL;
-        A = __fadd_rn(A, zc == EPSL ? p.W : U(i, zc));
+        // next step's operands, all issued at once: node info of z_i, theta(z_{i-1} -> z_i),
+        // the candidate-range end of z_{i-1}; U(i, z_i) is summed next step (or after the loop)
+        const int4 nc = zc != EPSL ? __ldg(sc.ninfo + zc) : NOI;
+        const float th_next = (rb && zc != EPSL) ? __ldg(sc.theta_pad + nb.w + (zc - nb.y)) : 0.f;
+        const int hi_next = rb ? sc.first(nb.x + T) : 0;
+        A = __fadd_rn(A, u_pend);
+        u_pend = zc == EPSL ? p.W : U(i, zc);
         if (lane == 0 && zo) zo[i] = zc == EPSL ? -1 : sc.id[zc];
         za = zb;
         zb = zc;
+        na = nb;
+        nb = nc;
+        th_ab = th_next;
+        hi_a = hi_next;
     }
+    if (M >= 2) A = __fadd_rn(A, u_pend);
     if (lane == 0) {
         if (bt.E[kk]) bt.E[kk][d.out] = bst.v;
         if (bt.A[kk]) bt.A[kk][d.out] = A;

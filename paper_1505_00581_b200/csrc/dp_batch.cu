@@ -126,7 +126,7 @@ __host__ __device__ inline StageLayout item_layout(const WorkItem &w, int T, int
 // while one item is processed the copies of the next one land in the other stage),
 // the copy warp's frame minima, the Delta table and the control block.
 struct SmemPlan {
-    size_t stage[3], fw, dl, ctl, total;
+    size_t stage[3], fw, dl, sc, ctl, total;
     __host__ __device__ SmemPlan(const TileCaps &c, int T, int NM) {
         size_t o = 0;
         auto take = [&](size_t bytes) {
@@ -139,6 +139,7 @@ struct SmemPlan {
         stage[2] = c.NSTAGE > 2 ? take((size_t)c.STAGE) : stage[0];
         fw = take(sizeof(float) * (size_t)NM * (c.FT + T));
         dl = take(sizeof(float) * (size_t)NM * T);
+        sc = take(sizeof(float) * (size_t)NM * T);
         ctl = take(1024);  // item descriptors and layouts, mbarriers, counters
         total = o;
     }
@@ -148,7 +149,7 @@ struct SmemPlan {
 // Optional pipeline trace (HGM_TRACE=1): globaltimer stamps of CTA 0, one launch.
 __device__ unsigned long long *g_trace = nullptr;
 __device__ __forceinline__ void trace(int m, int ev) {
-    if (g_trace && blockIdx.x == 0 && m < 64) {
+    if (blockIdx.x == 0 && g_trace && m < 64) {  // (CTA 0 only reads the pointer)
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         g_trace[m * 8 + ev] = t;
@@ -225,9 +226,11 @@ __global__ void __launch_bounds__(KDP_BLOCK, HGM_KDP_MINB) k_dp_fused(SceneView 
     const int T = p.T;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
+    float *SCG = reinterpret_cast<float *>(smem + sp.sc);  // [T][NM] lambda2 |g_{i-1} - g| (state constants)
     for (int q = tid; q < T * NM; q += KDP_THREADS) {
         const int dt = q / NM, k = q - dt * NM;
         DL[q] = delta_term(p.l2, kc.c[k].x, dt);
+        SCG[q] = state_const(p.l2, kc.c[k].y, dt);
     }
     if (tid == 0) {
         for (int st = 0; st < 3; ++st) {
@@ -238,14 +241,19 @@ __global__ void __launch_bounds__(KDP_BLOCK, HGM_KDP_MINB) k_dp_fused(SceneView 
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    // PDL (launch_nm): let the next step's grid launch as our CTAs retire, and wait for the
+    // previous step's grid (its alpha layer, its (eps, eps) reset) before touching global data
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (warp == KDP_WARPS) {
         // ---------------- copy warp: item m goes to stage m % 2 once item m-2 left it; it
         // also computes the dummy-form states (eps, b) and (eps, eps) of each item
         // lane 0 claims one item ahead: the claim and the descriptor load of item m+1 are in
         // flight while item m-1 still occupies the stage item m+1 will use
         int next_idx = lane == 0 ? atomicAdd(counter, 1) : 0;
-        for (int m = 0;; ++m) {
-            const int st = m % nstage, use = m / nstage;  // use: how many items stage st held before
+        // st = m % nstage, use = m / nstage (how many items stage st held before), stepped
+        // incrementally: nstage is a runtime value and an integer division costs ~20 instructions
+        for (int m = 0, st = 0, use = 0;; ++m, st = (st + 1 == nstage) ? 0 : st + 1, use += st == 0 ? 1 : 0) {
             WorkItem pre{};
             if (lane == 0) {
                 if (next_idx < nitems) pre = items[next_idx];
@@ -318,8 +326,7 @@ __global__ void __launch_bounds__(KDP_BLOCK, HGM_KDP_MINB) k_dp_fused(SceneView 
         }
         return;
     }
-    for (int m = 0;; ++m) {
-        const int s = m % nstage, use = m / nstage;
+    for (int m = 0, s = 0, use = 0;; ++m, s = (s + 1 == nstage) ? 0 : s + 1, use += s == 0 ? 1 : 0) {
         if (tid == 0) trace(m, 0);
         mbar_wait(&ctl->raw[s], use & 1);
         if (tid == 0) trace(m, 1);
@@ -495,7 +502,7 @@ __global__ void __launch_bounds__(KDP_BLOCK, HGM_KDP_MINB) k_dp_fused(SceneView 
                 float out0[EPF], out1[EPF];
 #pragma unroll
                 for (int k = 0; k < NM; ++k) {
-                    const float sc_g = state_const(p.l2, kc.c[k].y, sg.g);  // same frame gap for both states
+                    const float sc_g = SCG[sg.g * NM + k];  // state_const(l2, g_{i-1}, g): same gap for both states
                     const float ean = b_ean[(b - B0) * NM + k];
                     out0[k] = fminf(__fadd_rn(R0[k], sc_g), ean);
                     out1[k] = fminf(__fadd_rn(R1[k], sc_g), ean);
@@ -731,8 +738,24 @@ static hgm_status launch_nm(const SceneView &v, const WorkItem *items, int nitem
         cudaMemset(tbuf, 0, 64 * 8 * 8);
         cudaMemcpyToSymbol(g_trace, &tbuf, sizeof(tbuf));
     }
-    kern<<<grid, KDP_BLOCK, smem, s>>>(v, items, nitems, counter, hist, L, layer, has_prev ? 1 : 0, kc, U,
-                                         ui_off, p, caps, book);
+    // Programmatic dependent launch: the CTAs of this step may become resident as soon as
+    // the previous step's CTAs retire (each triggers at its start), run their prologue (Delta
+    // table, mbarriers) and then wait in griddepcontrol.wait until the previous step's grid
+    // has completed and its alpha layer is visible -- the launch gap and the prologue leave
+    // the per-step critical path (many short steps: single instances, few-window chunks).
+    static const bool pdl = !(getenv("HGM_PDL") && atoi(getenv("HGM_PDL")) == 0);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(KDP_BLOCK);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    HGM_CUDA(cudaLaunchKernelEx(&cfg, kern, v, items, nitems, counter, hist, L, layer, has_prev ? 1 : 0, kc, U, ui_off,
+                                p, caps, book));
     if (tbuf) {
         unsigned long long h[64 * 8], *z = nullptr;
         cudaMemcpy(h, tbuf, sizeof(h), cudaMemcpyDeviceToHost);

@@ -39,7 +39,7 @@ namespace hgm {
 constexpr int KW_THREADS_MAX = 1024;
 
 struct WinPlan {  // shared-memory plan (byte offsets), sized by the launch's maxima
-    size_t th, ent, lay, ur, wc, bean, rmin, nt, nlo, nhi, nro, nfc, nlc, ftl, task, dl, kc, kca, ctl, total;
+    size_t th, ent, lay, ur, dn, wc, bean, nt, nlo, nhi, nro, nfc, nlc, ftl, task, dl, kc, kca, ctl, total;
     int lay_floats;
     __host__ __device__ WinPlan(const WinCaps &c, int NM) {
         size_t o = 0;
@@ -53,9 +53,9 @@ struct WinPlan {  // shared-memory plan (byte offsets), sized by the launch's ma
         ent = take(4 * (size_t)went_floats(NM) * c.NPP);
         lay = take(4 * (size_t)lay_floats);
         ur = take(4 * ((size_t)NM * c.SW + 8));
-        wc = take(4 * (size_t)NM * c.SW);
+        dn = take(4 * (size_t)NM * (2 * c.SW + 1));
+        wc = take(NM >= 3 ? 4 * (size_t)NM * c.SW : 0);
         bean = take(4 * (size_t)NM * c.SW);
-        rmin = take(4 * (size_t)NM * c.SW);
         nt = take(4 * (size_t)c.SW);
         nlo = take(4 * (size_t)c.SW);
         nhi = take(4 * (size_t)c.SW);
@@ -95,11 +95,13 @@ __device__ __forceinline__ int cta_excl_scan(int v, int *s_warp, int *total) {
 // Optional step trace (HGM_TRACE_W=1, diagnosis): globaltimer stamps of CTA 0 at the
 // phase boundaries of every step of one launch: [step][0..5]
 __device__ unsigned long long *g_wtrace = nullptr;
-__device__ __forceinline__ void wtrace(int s, int ev) {
-    if (g_wtrace && blockIdx.x == 0 && threadIdx.x == 0 && s < 256) {
+// (the pointer is read ONCE per kernel, by thread 0 of CTA 0: a global load per call site
+// stalled every step -- ncu attributed 9 % of K-DPW's stall samples to it)
+__device__ __forceinline__ void wtrace(unsigned long long *wt, int s, int ev) {
+    if (wt && s < 256) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        g_wtrace[s * 8 + ev] = t;
+        wt[s * 8 + ev] = t;
     }
 }
 
@@ -107,18 +109,23 @@ template <int NM, int KW_THREADS>
 __global__ void __launch_bounds__(KW_THREADS) k_dp_window(SceneView sc, const InstDesc *__restrict__ inst,
                                                            float *__restrict__ hist, int64_t L, int M,
                                                            WinStepPtrs sp, const float *__restrict__ U, int64_t nn,
-                                                           int64_t n_lo, DPParams p, WinCaps caps) {
+                                                           int64_t n_lo, DPParams p, WinCaps caps,
+                                                           const WinPlan pl) {
     constexpr int EPF = went_floats(NM);
     constexpr int KW_WARPS = KW_THREADS / 32;
+    // the (eps, x) dummy forms: in the row warps' pass (one more reduction per model and row)
+    // for small batches, else per (x, model) thread after the barrier from a per-node w table
+    constexpr bool kMergeDummy = NM <= 2;
     extern __shared__ __align__(128) unsigned char smem[];
-    const WinPlan pl(caps, NM);
+    // (the shared-memory plan comes in the parameter space, computed on the host: built
+    // here, its offsets were rematerialised inside the loops -- ~4 % of the instructions)
     float *TH = reinterpret_cast<float *>(smem + pl.th);
     float *ENT = reinterpret_cast<float *>(smem + pl.ent);
     float *LAY = reinterpret_cast<float *>(smem + pl.lay);
     float *UR = reinterpret_cast<float *>(smem + pl.ur);
-    float *WC = reinterpret_cast<float *>(smem + pl.wc);
+    float *DN = reinterpret_cast<float *>(smem + pl.dn);      // new dummy-form slots of the step
+    float *WC = reinterpret_cast<float *>(smem + pl.wc);      // w(c) per node (NM >= 3)
     float *BEAN = reinterpret_cast<float *>(smem + pl.bean);
-    float *RMIN = reinterpret_cast<float *>(smem + pl.rmin);
     int *NT = reinterpret_cast<int *>(smem + pl.nt);
     int *NLO = reinterpret_cast<int *>(smem + pl.nlo);
     int *NHI = reinterpret_cast<int *>(smem + pl.nhi);
@@ -137,6 +144,7 @@ __global__ void __launch_bounds__(KW_THREADS) k_dp_window(SceneView sc, const In
     int *s_warp = reinterpret_cast<int *>(smem + pl.ctl + 48);    // KW_WARPS + 1 ints
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    unsigned long long *const wt = (blockIdx.x == 0 && tid == 0) ? g_wtrace : nullptr;
     const InstDesc d = inst[blockIdx.x];
     const int wb = d.wb, Sw = d.we - d.wb, npp = d.npp, T = p.T, o = d.o, W = caps.W;
     const int EE = npp + 2 * Sw;  // (eps, eps) slot
@@ -196,13 +204,49 @@ __global__ void __launch_bounds__(KW_THREADS) k_dp_window(SceneView sc, const In
             }
         }
         if (tid == 0) *s_ntask = base;
+        // ---- tasks in descending order of their candidate counts (a counting sort by trip,
+        // once per window): the 32 lanes of a claimed group then run near-equal trips (the
+        // gap-major order leaves Poisson-spread trips in a group, and the loop runs as long
+        // as its longest lane).  Scratch: the entry area ENT, unused until the first step.
+        // Order within a trip is arbitrary: every task owns its states, so no result changes.
+        int *HIST = reinterpret_cast<int *>(ENT);                 // [Sw + 1] counts, then cursors
+        unsigned *TMP = reinterpret_cast<unsigned *>(ENT) + ((Sw + 4) & ~3);  // [ntask]
+        if ((size_t)((Sw + 4) & ~3) + (size_t)base <= (size_t)EPF * caps.NPP) {
+            auto trip_of = [&](unsigned tk) {
+                const int b = (int)(tk & 0xffffu), a0 = (int)((tk >> 16) & 0x7fffu);
+                return min(Sw, max(0, NHI[a0] - NLO[b]));
+            };
+            for (int q = tid; q <= Sw; q += KW_THREADS) HIST[q] = 0;
+            __syncthreads();
+            for (int q = tid; q < base; q += KW_THREADS) {
+                const unsigned tk = TASK[q];
+                TMP[q] = tk;
+                atomicAdd(&HIST[trip_of(tk)], 1);
+            }
+            __syncthreads();
+            int carry = 0;  // first position of trip v = the tasks of trips > v
+            for (int r0 = 0; r0 <= Sw; r0 += KW_THREADS) {
+                const int r = r0 + tid, v = Sw - r;
+                const int cnt = r <= Sw ? HIST[v] : 0;
+                int tot;
+                const int ex = cta_excl_scan<KW_WARPS>(cnt, s_warp, &tot);
+                if (r <= Sw) HIST[v] = carry + ex;
+                carry += tot;
+            }
+            __syncthreads();
+            for (int q = tid; q < base; q += KW_THREADS) {
+                const unsigned tk = TMP[q];
+                TASK[atomicAdd(&HIST[trip_of(tk)], 1)] = tk;
+            }
+            __syncthreads();
+        }
     }
 
     int u_use = 0;
     for (int s = 0; s < nsteps; ++s) {
         const int i = M - 1 - s;  // 0-based model node of this step; layer i - 2
         const bool has_next = s > 0;
-        wtrace(s, 0);
+        wtrace(wt, s, 0);
         // ---- step constants (model gaps / angles) and the Delta table
         if (tid == 0) {
             StepConstB kc{};
@@ -219,35 +263,60 @@ __global__ void __launch_bounds__(KW_THREADS) k_dp_window(SceneView sc, const In
             const int dt = q / NM, k = q - dt * NM;
             DL[q] = delta_term(p.l2, KCA[i * NM + k].x, dt);
         }
+        // the new dummy-form slots (DN: (x, eps) | (eps, x) | (eps, eps)) are built apart from
+        // LAY (whose old ones phase 1 still reads); (eps, eps) starts at lambda1 W^d + its old
+        // value and is min-reduced by phase 1
+        if (tid < NM) {
+            const float een = __fadd_rn(p.l1W, has_next ? LAY[EE * NM + tid] : 0.f);
+            EEN[tid] = een;
+            DN[2 * Sw * NM + tid] = een;
+        }
         mbar_wait(ubar, u_use & 1);  // U_i landed
         ++u_use;
         const float *Ui = UR + (((int64_t)i * nn + (wb - n_lo)) * NM & 3);
         __syncthreads();
-        wtrace(s, 1);
-        // ---- phase 1: dummy-form terms per node, messages + (b, eps) minima per row
-        for (int q = tid; q < Sw * NM; q += KW_THREADS) {
-            const int c = q / NM, k = q - c * NM;
-            WC[q] = msg_n(has_next ? LAY[(npp + c) * NM + k] : 0.f, Ui[q]);             // w(c)
-            BEAN[q] = __fadd_rn(p.l1W, has_next ? LAY[(npp + Sw + c) * NM + k] : 0.f);        // eps candidate
+        wtrace(wt, s, 1);
+        // ---- phase 1 (one pass, no barrier inside):
+        // (eps, eps) = min(min over the window's nodes c of w(c), lambda1 W^d + alpha_{i+1}(eps, eps)),
+        // w(c) = alpha_{i+1}(c, eps) + lambda1 U_i(c): per warp a segmented minimum over the lanes
+        // of equal model index (lanes l, l + NM, l + 2 NM, ...), then one atomic per model (w >= 0)
+        for (int q0 = warp * 32; q0 < Sw * NM; q0 += KW_THREADS) {
+            const int q = q0 + lane;
+            float w = INFINITY;
+            if (q < Sw * NM) w = msg_n(has_next ? LAY[npp * NM + q] : 0.f, Ui[q]);
+            if constexpr (!kMergeDummy)
+                if (q < Sw * NM) WC[q] = w;
+            for (int o = NM; o < 32; o <<= 1) w = fminf(w, __shfl_down_sync(0xffffffffu, w, o));
+            if (lane < NM && q < Sw * NM)
+                atomicMin(reinterpret_cast<unsigned *>(DN + 2 * Sw * NM + (q0 + lane) % NM), __float_as_uint(w));
         }
-        if (tid < NM) EEN[tid] = __fadd_rn(p.l1W, has_next ? LAY[EE * NM + tid] : 0.f);
-        // messages + (b, eps) minima, one warp per b row (measured faster than groups of
-        // 4-16 lanes per row on short rows: the per-group redux.sync masks serialise)
+        // messages and every dummy form of row x, one warp per row (measured faster than groups
+        // of 4-16 lanes per row on short rows: the per-group redux.sync masks serialise):
+        //   m(x, c) = alpha_{i+1}(c, x) + lambda1 U_i(c) + lambda2 Delta -> ENT, with theta(x -> c)
+        //   (x, eps) = min(min_c n(x, c), lambda1 W^d + alpha_{i+1}(eps, x))
+        //   (eps, x) = min(min_c w(c), lambda1 W^d + alpha_{i+1}(eps, eps)): the row's candidates
+        //   c are exactly the nodes of frames (t'x, t'x + T) in the window
         for (int x = warp; x < Sw; x += KW_WARPS) {
             const int c0 = NLO[x], len = NHI[x] - c0, ro = NRO[x], tx = NT[x];
-            float mn[NM];
+            float mn[NM], wm[NM];
 #pragma unroll
-            for (int k = 0; k < NM; ++k) mn[k] = INFINITY;
+            for (int k = 0; k < NM; ++k) mn[k] = wm[k] = INFINITY;
             for (int j = lane; j < len; j += 32) {
                 const int c = c0 + j, e = ro + j;
                 const float *dl = DL + (NT[c] - tx) * NM;
+                const float *uc = Ui + c * NM;
+                if constexpr (kMergeDummy) {
+#pragma unroll
+                    for (int k = 0; k < NM; ++k)
+                        wm[k] = fminf(wm[k], msg_n(has_next ? LAY[(npp + c) * NM + k] : 0.f, uc[k]));
+                }
                 float ent[EPF];
 #pragma unroll
                 for (int k = 0; k < NM; ++k) ent[k] = LAY[e * NM + k];  // alpha_{i+1}(c, x)
                 if (has_next)
-                    msg_build<NM, true>(ent, Ui + c * NM, dl, mn);
+                    msg_build<NM, true>(ent, uc, dl, mn);
                 else
-                    msg_build<NM, false>(ent, Ui + c * NM, dl, mn);
+                    msg_build<NM, false>(ent, uc, dl, mn);
                 ent[NM] = TH[e];
 #pragma unroll
                 for (int k = NM + 1; k < EPF; ++k) ent[k] = 0.f;
@@ -261,32 +330,41 @@ __global__ void __launch_bounds__(KW_THREADS) k_dp_window(SceneView sc, const In
                 }
             }
 #pragma unroll
-            for (int k = 0; k < NM; ++k) {  // n >= 0: float order = unsigned bit order
+            for (int k = 0; k < NM; ++k) {  // n, w >= 0: float order = unsigned bit order
                 const float v = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(mn[k])));
-                if (lane == k) RMIN[x * NM + k] = v;
+                float vw = 0.f;
+                if constexpr (kMergeDummy) vw = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(wm[k])));
+                if (lane == k) {
+                    const float bean = __fadd_rn(p.l1W, has_next ? LAY[(npp + Sw + x) * NM + k] : 0.f);
+                    BEAN[x * NM + k] = bean;                     // the eps candidate of the states (x, a)
+                    DN[x * NM + k] = fminf(v, bean);             // (x, eps)
+                    if constexpr (kMergeDummy) DN[(Sw + x) * NM + k] = fminf(vw, EEN[k]);  // (eps, x)
+                }
             }
         }
-        wtrace(s, 6);
+        wtrace(wt, s, 6);
         if (tid == 0) bulk_wait_read_all();  // the previous layer's bulk store has read LAY
-        wtrace(s, 7);
+        wtrace(wt, s, 7);
         __syncthreads();
-        wtrace(s, 2);
+        wtrace(wt, s, 2);
         if (tid == 0 && s + 1 < nsteps) issue_u(i - 1);  // UR is free: prefetch the next step's row
-        // ---- phase 2a: dummy-form states of step i (cheap; every thread)
-        for (int q = tid; q < Sw * NM; q += KW_THREADS) {
-            const int x = q / NM, k = q - x * NM;
-            LAY[(npp + x) * NM + k] = fminf(RMIN[q], BEAN[q]);  // (x, eps)
-            float r = INFINITY;
-            for (int c = NLO[x]; c < NHI[x]; ++c) r = fminf(r, WC[c * NM + k]);  // frames (t'x, t'x + T)
-            LAY[(npp + Sw + x) * NM + k] = fminf(r, EEN[k]);  // (eps, x)
+        // ---- the new dummy forms into LAY (phase 2b reads BEAN, never LAY's dummy slots)
+        if constexpr (kMergeDummy) {
+            for (int q = tid; q < (2 * Sw + 1) * NM; q += KW_THREADS) LAY[npp * NM + q] = DN[q];
+        } else {
+            // large batches (NM >= 3): the (eps, x) minima from the per-node w table, one thread per
+            // (x, model) scanning the row's candidate nodes, overlapping phase 2b (NM more row
+            // reductions per warp made the 50-model context rows slower on short rows)
+            for (int q = tid; q < Sw * NM; q += KW_THREADS) {
+                const int x = q / NM, k = q - x * NM;
+                float r = INFINITY;
+                for (int c = NLO[x]; c < NHI[x]; ++c) r = fminf(r, WC[c * NM + k]);  // frames (t'x, t'x + T)
+                LAY[(npp + Sw + x) * NM + k] = fminf(r, EEN[k]);
+                LAY[(npp + x) * NM + k] = DN[q];  // (x, eps)
+            }
+            if (tid < NM) LAY[(npp + 2 * Sw) * NM + tid] = DN[2 * Sw * NM + tid];  // (eps, eps)
         }
-        if (tid < NM) LAY[EE * NM + tid] = EEN[tid];  // (eps, eps) of step i starts here ...
-        __syncthreads();
-        wtrace(s, 3);
-        for (int q = tid; q < Sw * NM; q += KW_THREADS) {
-            const int k = q % NM;
-            atomicMin(reinterpret_cast<unsigned *>(LAY + EE * NM + k), __float_as_uint(WC[q]));  // ... and is min-reduced (w >= 0)
-        }
+        wtrace(wt, s, 3);
         // ---- phase 2b: real states, 32-task groups claimed by warps
         // Few tasks for the CTA's threads (small windows): LPT = 2 or 4 lanes share a task, each
         // taking a contiguous share of its candidates, and the shares' minima are combined by
@@ -363,10 +441,10 @@ __global__ void __launch_bounds__(KW_THREADS) k_dp_window(SceneView sc, const In
                 }
             }
         }
-        wtrace(s, 4);
+        wtrace(wt, s, 4);
         fence_async_smem();  // LAY's generic-proxy writes before the bulk store reads them
         __syncthreads();
-        wtrace(s, 5);
+        wtrace(wt, s, 5);
         if (tid == 0) {  // alpha_i -> the history (layer i - 2), one bulk store
             bulk_s2g(hist + (int64_t)(i - 2) * L + d.off, LAY, lay_bytes);
             bulk_commit();
@@ -402,7 +480,7 @@ static hgm_status launch_w(const SceneView &v, const InstDesc *dinst, int ninst,
         cudaMemset(tbuf, 0, 256 * 8 * 8);
         cudaMemcpyToSymbol(g_wtrace, &tbuf, sizeof(tbuf));
     }
-    k_dp_window<NM, NT><<<ninst, NT, smem, s>>>(v, dinst, hist, L, M, sp, U, nn, n_lo, p, caps);
+    k_dp_window<NM, NT><<<ninst, NT, smem, s>>>(v, dinst, hist, L, M, sp, U, nn, n_lo, p, caps, WinPlan(caps, NM));
     if (tbuf) {
         static unsigned long long h[256 * 8];
         unsigned long long *z = nullptr;

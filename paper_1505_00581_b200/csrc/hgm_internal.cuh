@@ -111,7 +111,14 @@ namespace hgm {
 
 // ------------------------------------------------------------------ profiling
 enum KClass { K_SCENE = 0, K_MODEL = 1, K_UNARY = 2, K_DP = 3, K_BT = 4, K_ARG = 5, K_MSG = 6 };
-struct Timer {  // CUDA events on the launch stream, only when profiling is on
+#include <nvtx3/nvToolsExt.h>
+
+struct NvtxRange {  // host range around an ABI call (no-op unless a tool is attached)
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
+struct Timer {  // CUDA events on the launch stream, only when profiling is on; always an NVTX range
     cudaStream_t s;
     int cls;
     cudaEvent_t a = nullptr, b = nullptr;

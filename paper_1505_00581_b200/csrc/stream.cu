@@ -60,6 +60,7 @@ hgm_status hgm_stream_create(const hgm_model *const *models, int32_t n_models, c
 
 hgm_status hgm_stream_push(hgm_stream *st, const hgm_points *pts, int32_t n_frames, int32_t capacity,
                            int32_t *winner, float *score, int32_t *n_out, int64_t *first_offset) {
+    NvtxRange nvtx_("hgm_stream_push");
     if (!st || !n_out || !first_offset) return fail(HGM_ERR_INVALID_ARGUMENT, "NULL argument");
     if (n_frames < 0) return fail(HGM_ERR_INVALID_ARGUMENT, "n_frames < 0");
     *n_out = 0;

@@ -47,6 +47,10 @@ __global__ void __launch_bounds__(KU_TN) k_unary(const float *__restrict__ mfeat
         float acc[KU_TJ][4];
 #pragma unroll
         for (int q = 0; q < KU_TJ; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.f;
+        // unrolled so that several scene-descriptor loads are in flight (a small scene
+        // launches few CTAs and each thread's loop is otherwise one load latency per float4);
+        // every accumulator still sums its k in order, so the table's bits do not change
+#pragma unroll 4
         for (int k = 0; k < F4; ++k) {
             const float4 v = __ldg(srow + k);
 #pragma unroll

@@ -17,7 +17,7 @@ hdr = None
 line = None
 fname = "?"
 for r in rows:
-    if r and r[0] == "File Name":
+    if r and r[0] in ("File Name", "File Path"):
         fname = r[1].rsplit("/", 1)[-1]
         continue
     if r and r[0] == "Line No":
