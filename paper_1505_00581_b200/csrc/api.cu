@@ -6,7 +6,13 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <chrono>
+#include <memory>
+#include <condition_variable>
+#include <functional>
 #include <mutex>
+#include <thread>
+#include <vector>
 
 #include "hgm_internal.cuh"
 
@@ -65,6 +71,39 @@ cudaEvent_t take_event() {  // g_mu held
 }  // namespace
 
 bool profiling() { return g_prof; }
+
+static const char *const kHostSlot[] = {"detect call", "  per batch (run_batch)", "    unary alloc+launch",
+                                         "    match: plan", "    match: uploads", "    match: K-DP launches",
+                                         "    match: K-BT launches", "  lanes fork/join"};
+static double g_hp_us[HP_NSLOT];
+static long long g_hp_n[HP_NSLOT];
+static void hostprof_print() {
+    fprintf(stderr, "HGM_HOSTPROF host enqueue time per slot (total us, calls, us per call)\n");
+    for (int k = 0; k < HP_NSLOT; ++k)
+        if (g_hp_n[k])
+            fprintf(stderr, "  %-28s %10.1f %8lld %8.2f\n", kHostSlot[k], g_hp_us[k], g_hp_n[k], g_hp_us[k] / g_hp_n[k]);
+}
+bool hostprof_on() {
+    static const bool on = [] {
+        const bool e = getenv("HGM_HOSTPROF") && atoi(getenv("HGM_HOSTPROF")) > 0;
+        if (e) atexit(hostprof_print);
+        return e;
+    }();
+    return on;
+}
+static long long now_ns() {
+    return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+void hostprof_add(int slot, double us) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_hp_us[slot] += us;
+    g_hp_n[slot] += 1;
+}
+HostPhase::HostPhase(int s) : slot(s), t0(hostprof_on() ? now_ns() : 0) {}
+HostPhase::~HostPhase() {
+    if (t0) hostprof_add(slot, (now_ns() - t0) * 1e-3);
+}
 
 // NVTX ranges (SURVEY.md §5 tracing): every phase timer also opens a host range named after
 // its kernel class, so an nsys / ncu --nvtx timeline shows the scene build, unary table,
@@ -404,7 +443,9 @@ hgm_status hgm_match_model_at_offsets(const hgm_model *model, const hgm_scene *s
     DevBuf U, dE, dA, dz;
     const int64_t ustr = unary_stride(model->M, 1, nn);  // raw U, then lambda1 U
     HGM_TRY(U.alloc(sizeof(float) * 2 * (size_t)ustr, s));
-    HGM_TRY(unary_table(model->feat, model->M, 1, model->Fp, scene, n_lo, n_hi, params->lambda1, U.as<float>(),
+    ModelFeats mf1{};
+    mf1.p[0] = model->feat;
+    HGM_TRY(unary_table(mf1, model->M, 1, model->Fp, scene, n_lo, n_hi, params->lambda1, U.as<float>(),
                         U.as<float>() + ustr, s));
     const bool hE = E && !is_device_ptr(E), hA = A && !is_device_ptr(A), hz = z && !is_device_ptr(z);
     if (hE) HGM_TRY(dE.alloc(sizeof(float) * count, s));
@@ -429,6 +470,7 @@ hgm_status hgm_match_model_at_offsets(const hgm_model *model, const hgm_scene *s
 static hgm_status run_batch(const hgm_model *const *models, int m0, int m1, const hgm_scene *scene,
                             const hgm_params *params, const hgm_offsets *offsets, int64_t n_lo, int64_t n_hi,
                             float *Ed, float *Ad, int64_t *zb, int Mmax, cudaStream_t s, int lane) {
+    HostPhase hp_batch(HP_BATCH);
     const int count = offsets->count, Fp = scene->Fp;
     const int64_t nn = std::max<int64_t>(n_hi - n_lo, 1);
     const hgm_params pe = effective_params(params, scene);
@@ -436,15 +478,15 @@ static hgm_status run_batch(const hgm_model *const *models, int m0, int m1, cons
     for (int a = m0; a < m1;) {
         const int b = std::min(m1, a + max_batch);
         const int NM = b - a, M = models[a]->M;
-        DevBuf mfeat, U;
-        HGM_TRY(mfeat.alloc(sizeof(float) * (size_t)NM * M * Fp, s));
-        for (int k = 0; k < NM; ++k)
-            HGM_CUDA(cudaMemcpyAsync(mfeat.as<float>() + (size_t)k * M * Fp, models[a + k]->feat,
-                                     sizeof(float) * (size_t)M * Fp, cudaMemcpyDeviceToDevice, s));
+        std::unique_ptr<HostPhase> hp_u(new HostPhase(HP_UNARY));
+        DevBuf U;
+        ModelFeats mf{};  // K-U reads each model's descriptors in place (no gather copies per batch)
+        for (int k = 0; k < NM; ++k) mf.p[k] = models[a + k]->feat;
         const int64_t ustr = unary_stride(M, NM, nn);  // raw U, then lambda1 U
         HGM_TRY(U.alloc(sizeof(float) * 2 * (size_t)ustr, s));
-        HGM_TRY(unary_table(mfeat.as<float>(), M, NM, Fp, scene, n_lo, n_hi, params->lambda1, U.as<float>(),
+        HGM_TRY(unary_table(mf, M, NM, Fp, scene, n_lo, n_hi, params->lambda1, U.as<float>(),
                             U.as<float>() + ustr, s));
+        hp_u.reset();
         MatchOut mo[MAX_BATCH_API];
         for (int k = 0; k < NM; ++k)
             mo[k] = MatchOut{Ed + (size_t)(a + k) * count, Ad + (size_t)(a + k) * count, zb + (size_t)k * count * Mmax};
@@ -462,6 +504,75 @@ static hgm_status run_batch(const hgm_model *const *models, int m0, int m1, cons
     return HGM_OK;
 }
 
+// Host worker pool for the concurrent model batches of a detect call: each lane's enqueue
+// (allocations, planning, ~10 CUDA runtime calls per batch, ~50 us of host time: HGM_HOSTPROF)
+// runs on its own host thread, so a call with 7 batches enqueues in about one batch's time.
+// Workers are created once and park on a condition variable; lane 0 runs on the caller.  A
+// call that finds the pool busy (another host thread's detect) enqueues its lanes serially.
+class LanePool {
+  public:
+    ~LanePool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto &t : th_) t.join();
+    }
+    // fn(0) on the calling thread, fn(1..n-1) on workers; returns when all are done
+    void run(int n, const std::function<void(int)> &fn) {
+        std::unique_lock<std::mutex> busy(run_mu_, std::try_to_lock);
+        if (!busy.owns_lock() || n <= 1) {
+            for (int l = 0; l < n; ++l) fn(l);
+            return;
+        }
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            while ((int)th_.size() < n - 1) th_.emplace_back([this] { work(); });
+            job_ = &fn;
+            next_ = 1;
+            njob_ = n;
+            pending_ = n - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        fn(0);
+        std::unique_lock<std::mutex> lk(mu_);
+        done_.wait(lk, [this] { return pending_ == 0; });
+        job_ = nullptr;
+    }
+
+  private:
+    void work() {
+        uint64_t seen = 0;
+        std::unique_lock<std::mutex> lk(mu_);
+        for (;;) {
+            cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+            if (stop_) return;
+            seen = gen_;
+            while (job_ && next_ < njob_) {
+                const int l = next_++;
+                const std::function<void(int)> *fn = job_;
+                lk.unlock();
+                (*fn)(l);
+                lk.lock();
+                if (--pending_ == 0) done_.notify_all();
+            }
+        }
+    }
+    std::mutex run_mu_, mu_;
+    std::condition_variable cv_, done_;
+    std::vector<std::thread> th_;
+    const std::function<void(int)> *job_ = nullptr;
+    int next_ = 0, njob_ = 0, pending_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+static LanePool &lane_pool() {
+    static LanePool *p = new LanePool();  // never destroyed: workers may outlive static teardown order
+    return *p;
+}
+
 // E* and A of every (model, offset) into device matrices Ed / Ad [n_models][count].
 // Consecutive models of equal chain length form batches of up to MAX_BATCH_API (one K-DP
 // pass each).  When the call has few windows (count < 2 x SMs: one batch cannot fill the
@@ -471,6 +582,7 @@ static hgm_status run_batch(const hgm_model *const *models, int m0, int m1, cons
 static hgm_status detect_scores(const hgm_model *const *models, int32_t n_models, const hgm_scene *scene,
                                 const hgm_params *params, const hgm_offsets *offsets, float *Ed, float *Ad,
                                 cudaStream_t s) {
+    HostPhase hp_call(HP_CALL);
     const int count = offsets->count;
     configure_pool();
     int64_t n_lo, n_hi;
@@ -504,11 +616,26 @@ static hgm_status detect_scores(const hgm_model *const *models, int32_t n_models
         HGM_CUDA(cudaEventRecord(fork, s));
         hgm_status st = HGM_OK;
         for (int l = 0; l < nlane; ++l) HGM_CUDA(cudaStreamWaitEvent(aux_stream(scene->device, 1 + l), fork, 0));
-        for (int bi = 0; bi < nb && st == HGM_OK; ++bi) {
-            const int l = bi % nlane;
-            st = run_batch(models, batches[bi].first, batches[bi].second, scene, params, offsets, n_lo, n_hi, Ed, Ad,
-                           zb.as<int64_t>() + zlane * l, Mmax, aux_stream(scene->device, 1 + l), 1 + l);
-        }
+        // lane l enqueues batches l, l + nlane, ... on its stream, each lane from its own host
+        // thread (LanePool); a failing lane stops, its status and message are handed back
+        std::vector<hgm_status> lst((size_t)nlane, HGM_OK);
+        std::vector<std::string> lmsg((size_t)nlane);
+        const int dev = scene->device;
+        lane_pool().run(nlane, [&](int l) {
+            cudaSetDevice(dev);
+            for (int bi = l; bi < nb; bi += nlane) {
+                const hgm_status bs = run_batch(models, batches[bi].first, batches[bi].second, scene, params, offsets,
+                                                n_lo, n_hi, Ed, Ad, zb.as<int64_t>() + zlane * l, Mmax,
+                                                aux_stream(dev, 1 + l), 1 + l);
+                if (bs != HGM_OK) {
+                    lst[(size_t)l] = bs;
+                    lmsg[(size_t)l] = g_err;
+                    break;
+                }
+            }
+        });
+        for (int l = 0; l < nlane && st == HGM_OK; ++l)
+            if (lst[(size_t)l] != HGM_OK) st = fail(lst[(size_t)l], lmsg[(size_t)l]);
         for (int l = 0; l < nlane; ++l) {  // join (also after a failure: nothing may outlive the call's buffers)
             cudaEventCreateWithFlags(&join[l], cudaEventDisableTiming);
             cudaEventRecord(join[l], aux_stream(scene->device, 1 + l));
@@ -680,7 +807,10 @@ hgm_status hgm_get_stats(hgm_stats *out, int reset) {
     }
     g_pending.clear();
     *out = g_stats;
-    if (reset) g_stats = hgm_stats{};
+    if (reset) {
+        g_stats = hgm_stats{};
+        for (int k = 0; k < HP_NSLOT; ++k) g_hp_us[k] = 0.0, g_hp_n[k] = 0;  // (the host profile restarts too)
+    }
     return HGM_OK;
 }
 

@@ -203,6 +203,7 @@ __global__ void __launch_bounds__(256) k_backtrack(SceneView sc, const InstDesc 
         const bool co_ab = rb && ra && isnan(th_ab);
         const int aoff = ra ? c0 - na.y : 0;
         const int qbp = nb.w - d.ppad, tb = nb.x;
+        HGM_DCHECK(c0 >= d.wb && c1 <= d.we && (!rb || c1 <= c0 || (qbp >= 0 && qbp + (c1 - c0) <= d.npp)));
         // the dummy candidate's value does not depend on the real ones: its load goes first
         const float eps_nx = rb ? a_ea(nx, zb) : a_ee(nx);  // alpha_{i+1}(eps, b) or (eps, eps)
         auto value = [&](int c) -> float {

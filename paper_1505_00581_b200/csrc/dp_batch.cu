@@ -176,7 +176,8 @@ template <int NM, bool kHasNext>
 __device__ __forceinline__ void issue_stage(const SceneView &sc, WorkItem &w, const float *hist,
                                             int64_t L, int layer, const float *__restrict__ U, int64_t ui_off, int T,
                                             const SmemPlan &sp, unsigned char *smem, int s, uint64_t *bar,
-                                            const unsigned char *__restrict__ book, unsigned book_bytes) {
+                                            const unsigned char *__restrict__ book, unsigned book_bytes,
+                                            bool dep_wait) {
     constexpr int EPF = entry_floats(NM);
     const InstDesc &d = w.d;
     const StageLayout ly = item_layout(w, T, NM, (int)book_bytes);
@@ -184,15 +185,7 @@ __device__ __forceinline__ void issue_stage(const SceneView &sc, WorkItem &w, co
     Copier cl(bar);
     const int64_t nxo = (int64_t)(layer + 1) * L + d.off;  // alpha layer i+1 of this window (from the aligned base)
     const int Sw = d.we - d.wb;
-    if (kHasNext) {
-        cl.range(sb + ly.en, hist, nxo + (int64_t)(w.qb0 - d.ppad) * EPF, nxo + (int64_t)(w.qb1 - d.ppad) * EPF);
-        w.we0 = cl.range(sb + ly.we, hist, nxo + (int64_t)(d.ntail + w.B0 - d.wb) * EPF,
-                         nxo + (int64_t)(d.ntail + w.Cend - d.wb) * EPF);
-        w.eb0 = cl.range(sb + ly.eb, hist, nxo + (int64_t)(d.ntail + Sw + w.B0 - d.wb) * EPF,
-                         nxo + (int64_t)(d.ntail + Sw + w.B1 - d.wb) * EPF);
-        w.ee0 = cl.range(sb + ly.ee, hist, nxo + (int64_t)(d.ntail + 2 * Sw) * EPF,
-                         nxo + (int64_t)(d.ntail + 2 * Sw + 1) * EPF);
-    }
+    // step-independent inputs first (scene index, unary row, bookkeeping) ...
     w.th0 = w.qa - cl.range(sb + ly.th, sc.theta_pad, w.qa, w.qa1);  // TH[q] holds theta_pad[th0 + q]
     w.tb0 = cl.range(sb + ly.tb, sc.theta_pad, w.qb0, w.qb1);         // theta(b -> c) of the b rows' entries
     w.uc0 = cl.range(sb + ly.uc, U, ui_off + (int64_t)w.B0 * NM, ui_off + (int64_t)w.Cend * NM);
@@ -202,6 +195,18 @@ __device__ __forceinline__ void issue_stage(const SceneView &sc, WorkItem &w, co
     const int f_lo = max(0, w.F0 - T), f_hi = min(sc.fmax + 1, w.F1 + T);  // first_tab over [F0 - T, F1 + T]
     w.ft0 = cl.range(sb + ly.ftab, sc.ft, f_lo, f_hi + 1);
     w.flo = f_lo;
+    // ... then the alpha layer i+1, which the previous step's grid writes: under programmatic
+    // dependent launch the first item's static copies are in flight before this wait
+    if (dep_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (kHasNext) {
+        cl.range(sb + ly.en, hist, nxo + (int64_t)(w.qb0 - d.ppad) * EPF, nxo + (int64_t)(w.qb1 - d.ppad) * EPF);
+        w.we0 = cl.range(sb + ly.we, hist, nxo + (int64_t)(d.ntail + w.B0 - d.wb) * EPF,
+                         nxo + (int64_t)(d.ntail + w.Cend - d.wb) * EPF);
+        w.eb0 = cl.range(sb + ly.eb, hist, nxo + (int64_t)(d.ntail + Sw + w.B0 - d.wb) * EPF,
+                         nxo + (int64_t)(d.ntail + Sw + w.B1 - d.wb) * EPF);
+        w.ee0 = cl.range(sb + ly.ee, hist, nxo + (int64_t)(d.ntail + 2 * Sw) * EPF,
+                         nxo + (int64_t)(d.ntail + 2 * Sw + 1) * EPF);
+    }
     cl.close();  // (the stage was released by the consumers' empty[s] arrivals, after their reads)
 }
 
@@ -241,10 +246,14 @@ __global__ void __launch_bounds__(KDP_BLOCK, HGM_KDP_MINB) k_dp_fused(SceneView 
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    // PDL (launch_nm): let the next step's grid launch as our CTAs retire, and wait for the
-    // previous step's grid (its alpha layer, its (eps, eps) reset) before touching global data
+    // PDL (launch_nm): let the next step's grid launch as our CTAs retire.  The copy warp is
+    // the one that touches data of the previous step's grid (the alpha layer i+1 it
+    // bulk-copies, the (eps, eps) slot that grid reset): it waits (griddepcontrol.wait) only
+    // after claiming its first item and issuing that item's step-independent copies.  The
+    // compute warps read nothing but the stages; they wait here too, which parks them in
+    // hardware instead of polling the first stage's mbarrier while the previous grid runs.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (warp < KDP_WARPS) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (warp == KDP_WARPS) {
         // ---------------- copy warp: item m goes to stage m % 2 once item m-2 left it; it
         // also computes the dummy-form states (eps, b) and (eps, eps) of each item
@@ -272,13 +281,14 @@ __global__ void __launch_bounds__(KDP_BLOCK, HGM_KDP_MINB) k_dp_fused(SceneView 
                                  "r"((unsigned)(nw.B1 - nw.B0))
                                  : "memory");
                     issue_stage<NM, kHasNext>(sc, nw, hist, L, layer, U, ui_off, T, sp, smem, st, &ctl->raw[st], book,
-                                              (unsigned)bp.total);
+                                              (unsigned)bp.total, m == 0);
                     trace(m, 5);
                 } else {
                     nw.live = 0;
                     mbar_arrive(&ctl->raw[st]);
                 }
             }
+            if (m == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // (every lane: the dummy forms below)
             mbar_wait(&ctl->raw[st], use & 1);
             if (lane == 0) trace(m, 6);
             const WorkItem &w = ctl->w[st];
@@ -498,6 +508,8 @@ __global__ void __launch_bounds__(KDP_BLOCK, HGM_KDP_MINB) k_dp_fused(SceneView 
                     R1[k] = fminf(R1[k], __shfl_xor_sync(0xffffffffu, R1[k], o));
                 }
             }
+            HGM_DCHECK(!live || (ra0 >= 0 && ra1 < w.nA + NBr && rbt < w.nA + NBr && r_qp[ra0] + colb >= d.ppad &&
+                                 r_qp[ra1] + colb < d.ppad + d.npp && r_en[rbt] + trip <= w.qb1 - w.qb0 + 8));
             if (live && sub == 0) {
                 float out0[EPF], out1[EPF];
 #pragma unroll
@@ -732,7 +744,8 @@ static hgm_status launch_nm(const SceneView &v, const WorkItem *items, int nitem
     const int grid = std::max(1, std::min(nitems, std::max(1, bps) * nsm));
     static int traced = 0;
     unsigned long long *tbuf = nullptr;
-    if (getenv("HGM_TRACE") && !traced && layer == 10) {
+    static const bool trace_env = getenv("HGM_TRACE") != nullptr;  // (read once: this runs per launch)
+    if (trace_env && !traced && layer == 10) {
         traced = 1;
         cudaMalloc(&tbuf, 64 * 8 * 8);
         cudaMemset(tbuf, 0, 64 * 8 * 8);

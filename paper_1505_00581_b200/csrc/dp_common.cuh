@@ -1,9 +1,29 @@
 // dp_common.cuh -- types shared by the K-DP / K-BT kernels (dp.cu, dp_batch.cu, backtrack.cu).
 #pragma once
+#include <cstdio>
 #include "hgm_device.cuh"
 #include "hgm_internal.cuh"
 
 namespace hgm {
+
+// Device-side bounds checks of the shared-memory and history indices (built with
+// -DHGM_DEBUG_CHECKS: tests/test_gpu_debug_checks.py).  compute-sanitizer is closed on this
+// pool, so the kernels check their own indices: a failed check prints and traps (the call
+// then returns HGM_ERR_CUDA).
+#ifdef HGM_DEBUG_CHECKS
+#define HGM_DCHECK(cond)                                                                                    \
+    do {                                                                                                    \
+        if (!(cond)) {                                                                                      \
+            printf("HGM_DCHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, (int)blockIdx.x, \
+                   (int)threadIdx.x, #cond);                                                                \
+            __trap();                                                                                       \
+        }                                                                                                   \
+    } while (0)
+#else
+#define HGM_DCHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
 
 struct SceneView {
     const int32_t *__restrict__ t;

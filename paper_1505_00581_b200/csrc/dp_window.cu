@@ -196,6 +196,7 @@ __global__ void __launch_bounds__(KW_THREADS) k_dp_window(SceneView sc, const In
                 const int nt = (na + 1) >> 1;
                 int tot;
                 const int at = base + cta_excl_scan<KW_WARPS>(nt, s_warp, &tot);
+                HGM_DCHECK(at + nt <= caps.NTASK);
                 for (int q = 0; q < nt; ++q) {
                     const int a0 = a_lo + 2 * q;
                     TASK[at + q] = (unsigned)b | ((unsigned)a0 << 16) | (a0 + 1 < a_lo + na ? 0x80000000u : 0u);
@@ -303,6 +304,7 @@ __global__ void __launch_bounds__(KW_THREADS) k_dp_window(SceneView sc, const In
             for (int k = 0; k < NM; ++k) mn[k] = wm[k] = INFINITY;
             for (int j = lane; j < len; j += 32) {
                 const int c = c0 + j, e = ro + j;
+                HGM_DCHECK(c > x && c < Sw && e < npp && NT[c] - tx >= 1 && NT[c] - tx < T);
                 const float *dl = DL + (NT[c] - tx) * NM;
                 const float *uc = Ui + c * NM;
                 if constexpr (kMergeDummy) {
@@ -387,6 +389,8 @@ __global__ void __launch_bounds__(KW_THREADS) k_dp_window(SceneView sc, const In
             const int a1 = two ? a0 + 1 : a0;
             const int c0 = NLO[b], la = NLO[a0];
             const int trip = live ? NHI[a0] - c0 : 0;
+            HGM_DCHECK(!live || (a0 < b && a1 < b && b < Sw && NRO[a1] + (b - la) < npp && NRO[b] + max(trip, 0) <= npp &&
+                                 NRO[a0] + (c0 - la) + max(trip, 0) <= npp && NRO[a1] + (c0 - la) + max(trip, 0) <= npp));
             const int aoff = c0 - la, colb = b - la;
             const int ra0 = NRO[a0], ra1 = NRO[a1];
             const float *erow = ENT + (size_t)NRO[b] * EPF;
@@ -474,7 +478,8 @@ static hgm_status launch_w(const SceneView &v, const InstDesc *dinst, int ninst,
     }
     static int traced = 0;
     unsigned long long *tbuf = nullptr;
-    if (getenv("HGM_TRACE_W") && !traced) {  // diagnosis: per-step phase times of CTA 0, first launch
+    static const bool trace_env = getenv("HGM_TRACE_W") != nullptr;  // (read once: this runs per launch)
+    if (trace_env && !traced) {  // diagnosis: per-step phase times of CTA 0, first launch
         traced = 1;
         cudaMalloc(&tbuf, 256 * 8 * 8);
         cudaMemset(tbuf, 0, 256 * 8 * 8);

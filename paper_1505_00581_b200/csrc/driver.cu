@@ -84,10 +84,48 @@ struct Scratch {
         return HGM_OK;
     }
 };
+// Pinned host staging for a call's small uploads (window descriptors, item prefixes, frame
+// tiling): a copy from pageable memory is staged by the driver and can block the host for
+// tens of microseconds, which dominated the enqueue of few-window calls (50-model context
+// rows: 0.41 of 0.69 ms was host enqueue, tools/ctx_probe.py).  The buffer is reused once the
+// previous call's copies have read it (event).
+struct PinnedStage {
+    char *p = nullptr;
+    size_t cap = 0, used = 0;
+    cudaEvent_t read = nullptr;  // the last call's copies out of the buffer completed
+    hgm_status begin(size_t bytes) {
+        if (read) HGM_CUDA(cudaEventSynchronize(read));
+        else HGM_CUDA(cudaEventCreateWithFlags(&read, cudaEventDisableTiming));
+        if (bytes > cap) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            cap = 0;
+            const size_t want = std::max<size_t>(bytes, (size_t)1 << 16);
+            HGM_CUDA(cudaMallocHost(&p, want));
+            cap = want;
+        }
+        used = 0;
+        return HGM_OK;
+    }
+    // copy host bytes into the buffer and enqueue their transfer to dst on s
+    hgm_status put(void *dst, const void *src, size_t bytes, cudaStream_t s) {
+        if (!bytes) return HGM_OK;
+        memcpy(p + used, src, bytes);
+        HGM_CUDA(cudaMemcpyAsync(dst, p + used, bytes, cudaMemcpyHostToDevice, s));
+        used += (bytes + 15) & ~(size_t)15;
+        return HGM_OK;
+    }
+    hgm_status end(cudaStream_t s) {
+        HGM_CUDA(cudaEventRecord(read, s));
+        return HGM_OK;
+    }
+};
+
 struct ScratchSet {
     std::mutex mu;
     Scratch hist, items, book, counters;
     cudaEvent_t done = nullptr;
+    PinnedStage up;
 };
 // one set per (device, lane): lane 0 serves single-batch calls, lanes 1.. the concurrent
 // model batches of a detect call (each lane is one stream, so its set is never shared)
@@ -301,6 +339,7 @@ static bool window_path(const hgm_scene *sc, const std::vector<InstDesc> &all, i
 hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *sc, const hgm_params &pp,
                        const hgm_offsets &o, const float *U, const float *Us, int64_t n_lo, int64_t nn,
                        const MatchOut *outs, cudaStream_t s, int lane) {
+    std::unique_ptr<HostPhase> hp(new HostPhase(HP_PLAN));
     const int count = o.count, M = models[0]->M;
     if (count <= 0) return HGM_OK;
     if (NM < 1 || NM > MAX_BATCH) return fail(HGM_ERR_INVALID_ARGUMENT, "model batch size must be 1..8");
@@ -345,16 +384,8 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
     if (!v0 && !win) {
         HGM_TRY(d_subb.alloc(sizeof(int32_t) * tl.sub_begin.size(), s));
         HGM_TRY(d_subg.alloc(sizeof(int32_t) * std::max<size_t>(2, tl.sub_g.size()), s));
-        HGM_CUDA(cudaMemcpyAsync(d_subb.p, tl.sub_begin.data(), sizeof(int32_t) * tl.sub_begin.size(),
-                                 cudaMemcpyHostToDevice, s));
-        HGM_CUDA(cudaMemcpyAsync(d_subg.p, tl.sub_g.data(), sizeof(int32_t) * tl.sub_g.size(), cudaMemcpyHostToDevice,
-                                 s));
         HGM_TRY(d_gstart.alloc(sizeof(int32_t) * tl.gstart.size(), s));
         HGM_TRY(d_tile_of.alloc(sizeof(int32_t) * std::max<size_t>(1, tl.tile_of.size()), s));
-        HGM_CUDA(cudaMemcpyAsync(d_gstart.p, tl.gstart.data(), sizeof(int32_t) * tl.gstart.size(),
-                                 cudaMemcpyHostToDevice, s));
-        HGM_CUDA(cudaMemcpyAsync(d_tile_of.p, tl.tile_of.data(), sizeof(int32_t) * tl.tile_of.size(),
-                                 cudaMemcpyHostToDevice, s));
     }
     DPParams p;
     p.l1 = pp.lambda1;
@@ -442,19 +473,33 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
     }
     DevBuf d_all, d_ibase;
     HGM_TRY(d_all.alloc(sizeof(InstDesc) * count, s));
-    HGM_CUDA(cudaMemcpyAsync(d_all.p, all.data(), sizeof(InstDesc) * count, cudaMemcpyHostToDevice, s));
-    if (!v0 && !win) {
-        HGM_TRY(d_ibase.alloc(sizeof(int32_t) * (count + 1), s));
-        HGM_CUDA(cudaMemcpyAsync(d_ibase.p, ibase_all.data(), sizeof(int32_t) * (count + 1), cudaMemcpyHostToDevice, s));
+    if (!v0 && !win) HGM_TRY(d_ibase.alloc(sizeof(int32_t) * (count + 1), s));
+    ScratchSet &scr = scratch_set(sc->device, lane);
+    std::unique_lock<std::mutex> scr_lock(scr.mu);  // held while this call enqueues work on the buffers
+    hp.reset(new HostPhase(HP_UPLOAD));
+    {  // every small upload of the call through the lane's pinned staging buffer
+        const bool tiled = !v0 && !win;
+        size_t bytes = sizeof(InstDesc) * count + 16;
+        if (tiled)
+            bytes += 4 * (tl.sub_begin.size() + tl.sub_g.size() + tl.gstart.size() + tl.tile_of.size() + count + 1) + 80;
+        HGM_TRY(scr.up.begin(bytes));
+        HGM_TRY(scr.up.put(d_all.p, all.data(), sizeof(InstDesc) * count, s));
+        if (tiled) {
+            HGM_TRY(scr.up.put(d_ibase.p, ibase_all.data(), sizeof(int32_t) * (count + 1), s));
+            HGM_TRY(scr.up.put(d_subb.p, tl.sub_begin.data(), sizeof(int32_t) * tl.sub_begin.size(), s));
+            HGM_TRY(scr.up.put(d_subg.p, tl.sub_g.data(), sizeof(int32_t) * tl.sub_g.size(), s));
+            HGM_TRY(scr.up.put(d_gstart.p, tl.gstart.data(), sizeof(int32_t) * tl.gstart.size(), s));
+            HGM_TRY(scr.up.put(d_tile_of.p, tl.tile_of.data(), sizeof(int32_t) * tl.tile_of.size(), s));
+        }
+        HGM_TRY(scr.up.end(s));
     }
     if (nlanes == 2) {  // the second lane starts after the uploads
         HGM_CUDA(cudaEventRecord(ev_fork, s));
         HGM_CUDA(cudaStreamWaitEvent(lanes[1].s, ev_fork, 0));
     }
-    ScratchSet &scr = scratch_set(sc->device, lane);
-    std::unique_lock<std::mutex> scr_lock(scr.mu);  // held while this call enqueues work on the buffers
     if (!scr.done) HGM_CUDA(cudaEventCreateWithFlags(&scr.done, cudaEventDisableTiming));
     HGM_CUDA(cudaStreamWaitEvent(s, scr.done, 0));  // the previous user's kernels are done with them
+    hp.reset(new HostPhase(HP_DP));
     hgm_status st = HGM_OK;
     for (int chunk = 0; chunk < (int)chunks.size() && st == HGM_OK; ++chunk) {
         const Chunk &ch = chunks[chunk];
@@ -549,6 +594,7 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
             break;
         }
         {
+            HostPhase hp_bt(HP_BT);
             Timer tm(ls, K_BT);
             st = v0 ? launch_backtrack_v0(v, di, ninst, hist, L, bt, p, ls)
                     : launch_backtrack_warp(v, di, ninst, hist, L, bt, p, ls);

@@ -113,6 +113,18 @@ namespace hgm {
 enum KClass { K_SCENE = 0, K_MODEL = 1, K_UNARY = 2, K_DP = 3, K_BT = 4, K_ARG = 5, K_MSG = 6 };
 #include <nvtx3/nvToolsExt.h>
 
+// Host-side enqueue profile (diagnosis, HGM_HOSTPROF=1): wall time the host spends in each
+// part of a call, accumulated per slot and printed at process exit (tools/ctx_probe.py).
+enum HostSlot { HP_CALL = 0, HP_BATCH, HP_UNARY, HP_PLAN, HP_UPLOAD, HP_DP, HP_BT, HP_LANES, HP_NSLOT };
+bool hostprof_on();
+void hostprof_add(int slot, double us);
+struct HostPhase {
+    int slot;
+    long long t0;
+    explicit HostPhase(int s);
+    ~HostPhase();
+};
+
 struct NvtxRange {  // host range around an ABI call (no-op unless a tool is attached)
     explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
     ~NvtxRange() { nvtxRangePop(); }
@@ -135,7 +147,10 @@ hgm_status model_build_device(const hgm_points *dev_pts, int rank, cudaStream_t 
 // Unary table of a batch of NM models of M nodes each (model features stacked
 // model-major, node j = k*M + i), batched layout U[((i*nn) + (n - n_lo))*NM + k].
 // Us = lambda1 * U (same layout), the recursion's unary term
-hgm_status unary_table(const float *mfeat, int M, int NM, int Fp, const hgm_scene *sc, int64_t n_lo, int64_t n_hi,
+struct ModelFeats {  // the descriptor tables [M * Fp] of a batch's models (read in place by K-U)
+    const float *p[8];
+};
+hgm_status unary_table(const ModelFeats &mf, int M, int NM, int Fp, const hgm_scene *sc, int64_t n_lo, int64_t n_hi,
                        float l1, float *U, float *Us, cudaStream_t s);
 // floats of one table of M x nn x NM (+ 16 B of K-DP bulk-copy slack), 16-byte aligned:
 // the raw table at U, the scaled one at U + unary_stride(...)

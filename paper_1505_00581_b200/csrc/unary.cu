@@ -25,7 +25,7 @@ namespace hgm {
 constexpr int KU_TN = 128;  // scene nodes per CTA (one per thread)
 constexpr int KU_TJ = 8;    // model nodes per register tile
 
-__global__ void __launch_bounds__(KU_TN) k_unary(const float *__restrict__ mfeat, int M, int NM, int Fp,
+__global__ void __launch_bounds__(KU_TN) k_unary(ModelFeats mf, int M, int NM, int Fp,
                                                  const float *__restrict__ sfeat, int64_t n_lo, int64_t nn,
                                                  int tiles_per_y, float l1, float *__restrict__ U,
                                                  float *__restrict__ Us) {
@@ -41,8 +41,10 @@ __global__ void __launch_bounds__(KU_TN) k_unary(const float *__restrict__ mfeat
     for (int j0 = j_begin; j0 < j_end; j0 += KU_TJ) {
         const int nj = min(KU_TJ, j_end - j0);
         __syncthreads();
-        for (int k = threadIdx.x; k < nj * F4; k += KU_TN)
-            sm[k] = reinterpret_cast<const float4 *>(mfeat + (int64_t)j0 * Fp)[k];
+        for (int k = threadIdx.x; k < nj * F4; k += KU_TN) {  // node j = model kk's node i, read in place
+            const int q = k / F4, r = k - q * F4, j = j0 + q, kk = j / M, i = j - kk * M;
+            sm[k] = reinterpret_cast<const float4 *>(mf.p[kk] + (int64_t)i * Fp)[r];
+        }
         __syncthreads();
         float acc[KU_TJ][4];
 #pragma unroll
@@ -80,7 +82,7 @@ __global__ void __launch_bounds__(KU_TN) k_unary(const float *__restrict__ mfeat
     }
 }
 
-hgm_status unary_table(const float *mfeat, int M, int NM, int Fp, const hgm_scene *sc, int64_t n_lo, int64_t n_hi,
+hgm_status unary_table(const ModelFeats &mf, int M, int NM, int Fp, const hgm_scene *sc, int64_t n_lo, int64_t n_hi,
                        float l1, float *U, float *Us, cudaStream_t s) {
     const int64_t nn = n_hi - n_lo;
     if (nn <= 0 || M * NM <= 0) return HGM_OK;
@@ -91,7 +93,7 @@ hgm_status unary_table(const float *mfeat, int M, int NM, int Fp, const hgm_scen
     const int jt = (M * NM + KU_TJ - 1) / KU_TJ;                              // model-node tiles
     const int gy_want = (int)std::min<int64_t>(jt, std::max<int64_t>(1, (4 * 148 + gx - 1) / gx));
     const int tpy = (jt + gy_want - 1) / gy_want, gy = (jt + tpy - 1) / tpy;
-    k_unary<<<dim3((unsigned)gx, (unsigned)gy), KU_TN, smem, s>>>(mfeat, M, NM, Fp, sc->feat, n_lo, nn, tpy, l1, U, Us);
+    k_unary<<<dim3((unsigned)gx, (unsigned)gy), KU_TN, smem, s>>>(mf, M, NM, Fp, sc->feat, n_lo, nn, tpy, l1, U, Us);
     count_launch(K_UNARY);
     HGM_CUDA(cudaGetLastError());
     return HGM_OK;
