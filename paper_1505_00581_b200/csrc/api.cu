@@ -467,35 +467,41 @@ hgm_status hgm_match_model_at_offsets(const hgm_model *model, const hgm_scene *s
 // One model batch [m0, m1) of equal chain length on stream s (lane: its K-DP scratch set),
 // E* / A into Ed / Ad [n_models][count], assignments into the scratch zb.  A batch too
 // dense for a shared stage (g_tiling_failed) is retried one model at a time.
+// floats of a batch's unary region (raw + scaled tables), enough for the batch or for its
+// models one at a time (the dense-frame retry below)
+static int64_t unary_region(int M, int NM, int64_t nn) { return (2 * ((int64_t)M * NM * nn + 8 * NM) + 3) & ~(int64_t)3; }
+
 static hgm_status run_batch(const hgm_model *const *models, int m0, int m1, const hgm_scene *scene,
                             const hgm_params *params, const hgm_offsets *offsets, int64_t n_lo, int64_t n_hi,
-                            float *Ed, float *Ad, int64_t *zb, int Mmax, cudaStream_t s, int lane) {
+                            float *Ed, float *Ad, int64_t *zb, int Mmax, cudaStream_t s, int lane, float *ureg) {
     HostPhase hp_batch(HP_BATCH);
     const int count = offsets->count, Fp = scene->Fp;
     const int64_t nn = std::max<int64_t>(n_hi - n_lo, 1);
     const hgm_params pe = effective_params(params, scene);
     int max_batch = m1 - m0;
+    int64_t uoff = 0;  // next table in the batch's preallocated unary region (detect_scores)
     for (int a = m0; a < m1;) {
         const int b = std::min(m1, a + max_batch);
         const int NM = b - a, M = models[a]->M;
         std::unique_ptr<HostPhase> hp_u(new HostPhase(HP_UNARY));
-        DevBuf U;
         ModelFeats mf{};  // K-U reads each model's descriptors in place (no gather copies per batch)
         for (int k = 0; k < NM; ++k) mf.p[k] = models[a + k]->feat;
         const int64_t ustr = unary_stride(M, NM, nn);  // raw U, then lambda1 U
-        HGM_TRY(U.alloc(sizeof(float) * 2 * (size_t)ustr, s));
-        HGM_TRY(unary_table(mf, M, NM, Fp, scene, n_lo, n_hi, params->lambda1, U.as<float>(),
-                            U.as<float>() + ustr, s));
+        float *const Ut = ureg + uoff;  // raw U at Ut, lambda1 U at Ut + ustr
+        uoff += 2 * ustr;
+        HGM_TRY(unary_table(mf, M, NM, Fp, scene, n_lo, n_hi, params->lambda1, Ut,
+                            Ut + ustr, s));
         hp_u.reset();
         MatchOut mo[MAX_BATCH_API];
         for (int k = 0; k < NM; ++k)
             mo[k] = MatchOut{Ed + (size_t)(a + k) * count, Ad + (size_t)(a + k) * count, zb + (size_t)k * count * Mmax};
         g_tiling_failed = false;
         const hgm_status bst =
-            match_batch(models + a, NM, scene, pe, *offsets, U.as<float>(), U.as<float>() + ustr, n_lo, nn, mo, s, lane);
+            match_batch(models + a, NM, scene, pe, *offsets, Ut, Ut + ustr, n_lo, nn, mo, s, lane);
         if (bst != HGM_OK && g_tiling_failed && NM > 1) {
             if (getenv("HGM_DEBUG_TILING")) fprintf(stderr, "tiling: batch of %d retried one model at a time\n", NM);
             max_batch = 1;  // too dense for a batch's stage: one model at a time from here on
+            uoff = 0;       // (stream order: the retry's tables overwrite the failed batch's)
             continue;
         }
         HGM_TRY(bst);
@@ -603,13 +609,20 @@ static hgm_status detect_scores(const hgm_model *const *models, int32_t n_models
     const char *lenv = getenv("HGM_LANES");  // 1: batches one after another (tuning / tests)
     int nlane = (nb > 1 && !use_v0_kernels() && count < 2 * nsm) ? std::min(nb, MAX_LANES) : 1;
     if (lenv && atoi(lenv) >= 1) nlane = std::min({nb, MAX_LANES, atoi(lenv)});
-    DevBuf zb;
+    DevBuf zb, Uall;  // one allocation for every batch's unary tables (an allocation per batch
+                      // was ~20 us of host time each, and contended between the lanes' threads)
     const size_t zlane = (size_t)count * Mmax * MAX_BATCH_API;
     HGM_TRY(zb.alloc(sizeof(int64_t) * zlane * nlane, s));
+    const int64_t nn = std::max<int64_t>(n_hi - n_lo, 1);
+    std::vector<int64_t> uofs((size_t)nb + 1, 0);
+    for (int bi = 0; bi < nb; ++bi)
+        uofs[(size_t)bi + 1] = uofs[(size_t)bi] + unary_region(models[batches[bi].first]->M,
+                                                               batches[bi].second - batches[bi].first, nn);
+    HGM_TRY(Uall.alloc(sizeof(float) * (size_t)uofs[(size_t)nb], s));
     if (nlane == 1) {
         for (const auto &b : batches)
             HGM_TRY(run_batch(models, b.first, b.second, scene, params, offsets, n_lo, n_hi, Ed, Ad, zb.as<int64_t>(),
-                              Mmax, s, 0));
+                              Mmax, s, 0, Uall.as<float>() + uofs[(size_t)(&b - batches.data())]));
     } else {
         cudaEvent_t fork = nullptr, join[MAX_LANES] = {};
         HGM_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
@@ -626,7 +639,7 @@ static hgm_status detect_scores(const hgm_model *const *models, int32_t n_models
             for (int bi = l; bi < nb; bi += nlane) {
                 const hgm_status bs = run_batch(models, batches[bi].first, batches[bi].second, scene, params, offsets,
                                                 n_lo, n_hi, Ed, Ad, zb.as<int64_t>() + zlane * l, Mmax,
-                                                aux_stream(dev, 1 + l), 1 + l);
+                                                aux_stream(dev, 1 + l), 1 + l, Uall.as<float>() + uofs[(size_t)bi]);
                 if (bs != HGM_OK) {
                     lst[(size_t)l] = bs;
                     lmsg[(size_t)l] = g_err;

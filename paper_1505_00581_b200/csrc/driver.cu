@@ -123,7 +123,7 @@ struct PinnedStage {
 
 struct ScratchSet {
     std::mutex mu;
-    Scratch hist, items, book, counters;
+    Scratch hist, items, book, counters, desc;
     cudaEvent_t done = nullptr;
     PinnedStage up;
 };
@@ -380,13 +380,6 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
     }
     if (v0)
         for (InstDesc &d : all) d.ntail = d.np;  // v0 kernels: compact pair layout
-    DevBuf d_gstart, d_tile_of, d_subb, d_subg;
-    if (!v0 && !win) {
-        HGM_TRY(d_subb.alloc(sizeof(int32_t) * tl.sub_begin.size(), s));
-        HGM_TRY(d_subg.alloc(sizeof(int32_t) * std::max<size_t>(2, tl.sub_g.size()), s));
-        HGM_TRY(d_gstart.alloc(sizeof(int32_t) * tl.gstart.size(), s));
-        HGM_TRY(d_tile_of.alloc(sizeof(int32_t) * std::max<size_t>(1, tl.tile_of.size()), s));
-    }
     DPParams p;
     p.l1 = pp.lambda1;
     p.l2 = pp.lambda2;
@@ -471,25 +464,43 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
         HGM_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
         HGM_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     }
-    DevBuf d_all, d_ibase;
-    HGM_TRY(d_all.alloc(sizeof(InstDesc) * count, s));
-    if (!v0 && !win) HGM_TRY(d_ibase.alloc(sizeof(int32_t) * (count + 1), s));
     ScratchSet &scr = scratch_set(sc->device, lane);
     std::unique_lock<std::mutex> scr_lock(scr.mu);  // held while this call enqueues work on the buffers
+    if (!scr.done) HGM_CUDA(cudaEventCreateWithFlags(&scr.done, cudaEventDisableTiming));
+    HGM_CUDA(cudaStreamWaitEvent(s, scr.done, 0));  // the previous user's kernels are done with them
     hp.reset(new HostPhase(HP_UPLOAD));
-    {  // every small upload of the call through the lane's pinned staging buffer
+    // the call's small device arrays (window descriptors, item prefixes, frame tiling) live in
+    // the lane's cached descriptor scratch (no allocation per call) and are filled from its
+    // pinned staging buffer
+    InstDesc *d_all = nullptr;
+    int32_t *d_ibase = nullptr, *d_subb = nullptr, *d_subg = nullptr, *d_gstart = nullptr, *d_tile_of = nullptr;
+    {
         const bool tiled = !v0 && !win;
-        size_t bytes = sizeof(InstDesc) * count + 16;
-        if (tiled)
-            bytes += 4 * (tl.sub_begin.size() + tl.sub_g.size() + tl.gstart.size() + tl.tile_of.size() + count + 1) + 80;
-        HGM_TRY(scr.up.begin(bytes));
-        HGM_TRY(scr.up.put(d_all.p, all.data(), sizeof(InstDesc) * count, s));
+        auto rnd = [](size_t b) { return (b + 255) & ~(size_t)255; };
+        const size_t b_all = rnd(sizeof(InstDesc) * count), b_ib = tiled ? rnd(4 * ((size_t)count + 1)) : 0,
+                     b_sb = tiled ? rnd(4 * tl.sub_begin.size()) : 0,
+                     b_sg = tiled ? rnd(4 * std::max<size_t>(2, tl.sub_g.size())) : 0,
+                     b_gs = tiled ? rnd(4 * tl.gstart.size()) : 0,
+                     b_to = tiled ? rnd(4 * std::max<size_t>(1, tl.tile_of.size())) : 0;
+        HGM_TRY(scr.desc.ensure(b_all + b_ib + b_sb + b_sg + b_gs + b_to));
+        char *q = static_cast<char *>(scr.desc.p);
+        d_all = reinterpret_cast<InstDesc *>(q);
+        q += b_all;
         if (tiled) {
-            HGM_TRY(scr.up.put(d_ibase.p, ibase_all.data(), sizeof(int32_t) * (count + 1), s));
-            HGM_TRY(scr.up.put(d_subb.p, tl.sub_begin.data(), sizeof(int32_t) * tl.sub_begin.size(), s));
-            HGM_TRY(scr.up.put(d_subg.p, tl.sub_g.data(), sizeof(int32_t) * tl.sub_g.size(), s));
-            HGM_TRY(scr.up.put(d_gstart.p, tl.gstart.data(), sizeof(int32_t) * tl.gstart.size(), s));
-            HGM_TRY(scr.up.put(d_tile_of.p, tl.tile_of.data(), sizeof(int32_t) * tl.tile_of.size(), s));
+            d_ibase = reinterpret_cast<int32_t *>(q);
+            d_subb = reinterpret_cast<int32_t *>(q += b_ib);
+            d_subg = reinterpret_cast<int32_t *>(q += b_sb);
+            d_gstart = reinterpret_cast<int32_t *>(q += b_sg);
+            d_tile_of = reinterpret_cast<int32_t *>(q += b_gs);
+        }
+        HGM_TRY(scr.up.begin(b_all + b_ib + b_sb + b_sg + b_gs + b_to + 96));
+        HGM_TRY(scr.up.put(d_all, all.data(), sizeof(InstDesc) * count, s));
+        if (tiled) {
+            HGM_TRY(scr.up.put(d_ibase, ibase_all.data(), sizeof(int32_t) * (count + 1), s));
+            HGM_TRY(scr.up.put(d_subb, tl.sub_begin.data(), sizeof(int32_t) * tl.sub_begin.size(), s));
+            HGM_TRY(scr.up.put(d_subg, tl.sub_g.data(), sizeof(int32_t) * tl.sub_g.size(), s));
+            HGM_TRY(scr.up.put(d_gstart, tl.gstart.data(), sizeof(int32_t) * tl.gstart.size(), s));
+            HGM_TRY(scr.up.put(d_tile_of, tl.tile_of.data(), sizeof(int32_t) * tl.tile_of.size(), s));
         }
         HGM_TRY(scr.up.end(s));
     }
@@ -497,8 +508,6 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
         HGM_CUDA(cudaEventRecord(ev_fork, s));
         HGM_CUDA(cudaStreamWaitEvent(lanes[1].s, ev_fork, 0));
     }
-    if (!scr.done) HGM_CUDA(cudaEventCreateWithFlags(&scr.done, cudaEventDisableTiming));
-    HGM_CUDA(cudaStreamWaitEvent(s, scr.done, 0));  // the previous user's kernels are done with them
     hp.reset(new HostPhase(HP_DP));
     hgm_status st = HGM_OK;
     for (int chunk = 0; chunk < (int)chunks.size() && st == HGM_OK; ++chunk) {
@@ -519,7 +528,7 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
             }
             hist = ln.hist.as<float>();
         }
-        const InstDesc *di = d_all.as<InstDesc>() + k0;
+        const InstDesc *di = d_all + k0;
         const int nitems = ch.nitems;
         WorkItem *items_p = nullptr;
         int *counters_p = nullptr;
@@ -551,8 +560,8 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
                 book_p = ln.book.as<unsigned char>();
             }
             HGM_CUDA(cudaMemsetAsync(counters_p, 0, sizeof(int) * nsteps, ls));
-            launch_items(v, di, ninst, o.window, p.T, d_gstart.as<int32_t>(), d_tile_of.as<int32_t>(), tl.f_lo,
-                         d_subb.as<int32_t>(), d_subg.as<int32_t>(), d_ibase.as<int32_t>() + k0, ibase_all[k0], items_p,
+            launch_items(v, di, ninst, o.window, p.T, d_gstart, d_tile_of, tl.f_lo,
+                         d_subb, d_subg, d_ibase + k0, ibase_all[k0], items_p,
                          ls);
             launch_item_prep(v, items_p, nitems, tl.caps, p.T, book_p, ls);
             launch_init_ee(di, ninst, hist, L, nsteps - 1, NM, ls);  // first layer's (eps, eps) slots
