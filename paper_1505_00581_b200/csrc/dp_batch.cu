@@ -139,7 +139,10 @@ struct SmemPlan {
         stage[2] = c.NSTAGE > 2 ? take((size_t)c.STAGE) : stage[0];
         fw = take(sizeof(float) * (size_t)NM * (c.FT + T));
         dl = take(sizeof(float) * (size_t)NM * T);
-        sc = take(sizeof(float) * (size_t)NM * T);
+        // the state-constant table only for the T < 40 kernels (no task splitting): at large T its
+        // NM * T floats came out of the item stages and tipped dense C4 T = 80 batches into the
+        // one-model-at-a-time retry (2.4x slower); those kernels compute the constant inline
+        sc = take(T < 40 ? sizeof(float) * (size_t)NM * T : 0);
         ctl = take(1024);  // item descriptors and layouts, mbarriers, counters
         total = o;
     }
@@ -235,7 +238,7 @@ __global__ void __launch_bounds__(KDP_BLOCK, HGM_KDP_MINB) k_dp_fused(SceneView 
     for (int q = tid; q < T * NM; q += KDP_THREADS) {
         const int dt = q / NM, k = q - dt * NM;
         DL[q] = delta_term(p.l2, kc.c[k].x, dt);
-        SCG[q] = state_const(p.l2, kc.c[k].y, dt);
+        if constexpr (!kSplit) SCG[q] = state_const(p.l2, kc.c[k].y, dt);
     }
     if (tid == 0) {
         for (int st = 0; st < 3; ++st) {
@@ -514,7 +517,9 @@ __global__ void __launch_bounds__(KDP_BLOCK, HGM_KDP_MINB) k_dp_fused(SceneView 
                 float out0[EPF], out1[EPF];
 #pragma unroll
                 for (int k = 0; k < NM; ++k) {
-                    const float sc_g = SCG[sg.g * NM + k];  // state_const(l2, g_{i-1}, g): same gap for both states
+                    float sc_g;  // state_const(l2, g_{i-1}, g): same gap for both states
+                    if constexpr (!kSplit) sc_g = SCG[sg.g * NM + k];
+                    else sc_g = state_const(p.l2, kc.c[k].y, sg.g);
                     const float ean = b_ean[(b - B0) * NM + k];
                     out0[k] = fminf(__fadd_rn(R0[k], sc_g), ean);
                     out1[k] = fminf(__fadd_rn(R1[k], sc_g), ean);
@@ -710,7 +715,7 @@ template <int NM>
 static hgm_status launch_nm(const SceneView &v, const WorkItem *items, int nitems, const unsigned char *book,
                             int *counter, float *hist, int64_t L, int layer, bool has_next, bool has_prev,
                             const StepConstB &kc, const float *U, int64_t ui_off, const DPParams &p,
-                            const TileCaps &caps, cudaStream_t s) {
+                            const TileCaps &caps, cudaStream_t s, bool pdl_ok) {
     const size_t smem = dp_batch_smem(caps, p.T, NM);
     // task splitting (kSplit) only where trips can be long enough to split (T >= 40)
     const bool split = p.T >= 40;
@@ -756,7 +761,8 @@ static hgm_status launch_nm(const SceneView &v, const WorkItem *items, int nitem
     // table, mbarriers) and then wait in griddepcontrol.wait until the previous step's grid
     // has completed and its alpha layer is visible -- the launch gap and the prologue leave
     // the per-step critical path (many short steps: single instances, few-window chunks).
-    static const bool pdl = !(getenv("HGM_PDL") && atoi(getenv("HGM_PDL")) == 0);
+    static const bool pdl_env = !(getenv("HGM_PDL") && atoi(getenv("HGM_PDL")) == 0);  // HGM_PDL=0: off (A/B)
+    const bool pdl = pdl_env && pdl_ok;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(KDP_BLOCK);
@@ -789,11 +795,11 @@ static hgm_status launch_nm(const SceneView &v, const WorkItem *items, int nitem
 hgm_status launch_dp_batch(int NM, const SceneView &v, const WorkItem *items, int nitems, const unsigned char *book,
                            int *counter, float *hist, int64_t L, int layer, bool has_next, bool has_prev,
                            const StepConstB &kc, const float *U, int64_t ui_off, const DPParams &p,
-                           const TileCaps &caps, cudaStream_t s) {
+                           const TileCaps &caps, cudaStream_t s, bool pdl_ok) {
 #define HGM_NM_CASE(n)                                                                                             \
     case n:                                                                                                        \
         return launch_nm<n>(v, items, nitems, book, counter, hist, L, layer, has_next, has_prev, kc, U, ui_off, p, \
-                            caps, s)
+                            caps, s, pdl_ok)
     switch (NM) {
         HGM_NM_CASE(1);
         HGM_NM_CASE(2);

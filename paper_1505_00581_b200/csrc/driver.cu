@@ -19,7 +19,7 @@ size_t item_stage_bytes(int NE, int NTH, int NC, int NA, int NB, int FT, int T, 
 hgm_status launch_dp_batch(int NM, const SceneView &v, const WorkItem *items, int nitems, const unsigned char *book,
                            int *counter, float *hist, int64_t L, int layer, bool has_next, bool has_prev,
                            const StepConstB &kc, const float *U, int64_t ui_off, const DPParams &p,
-                           const TileCaps &caps, cudaStream_t s);
+                           const TileCaps &caps, cudaStream_t s, bool pdl_ok);
 hgm_status launch_items(const SceneView &v, const InstDesc *dinst, int ninst, int W, int T, const int32_t *gstart,
                         const int32_t *tile_of, int tf_lo, const int32_t *sub_begin, const int32_t *sub_g,
                         const int32_t *item_base, int base0, WorkItem *items, cudaStream_t s);
@@ -593,7 +593,8 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
                 kc.nK2[q] = make_float2(-kc.c[2 * q].w, -kc.c[k1].w);
             }
             st = launch_dp_batch(NM, v, items_p, nitems, book_p, counters_p + (i - 2), hist, L, i - 2, has_next,
-                                 /*has_prev=*/i - 1 >= 2, kc, Us, ((int64_t)i * nn - n_lo) * NM, p, tl.caps, ls);
+                                 /*has_prev=*/i - 1 >= 2, kc, Us, ((int64_t)i * nn - n_lo) * NM, p, tl.caps, ls,
+                                 /*pdl_ok=*/true);
             count_launch(K_DP);
         }
         dp_timer.reset();
