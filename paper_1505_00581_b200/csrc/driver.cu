@@ -393,7 +393,9 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
     // Windows are processed in chunks (the alpha history of a chunk must fit the
     // budget; a smaller chunk keeps a layer L2-resident for the next step's reads).
     // Optionally chunks alternate between two streams.
-    const int64_t budget_floats = (int64_t)3 << 29;  // alpha history per chunk: 6 GiB
+    // alpha history per chunk: 6 GiB (HGM_HIST_GB: tuning knob)
+    const char *genv = getenv("HGM_HIST_GB");
+    const int64_t budget_floats = ((genv && atoi(genv) > 0) ? (int64_t)atoi(genv) : 6) * ((int64_t)1 << 28);
     BTArgs bt{};
     bt.U = U;
     bt.Us = Us;
