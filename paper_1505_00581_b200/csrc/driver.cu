@@ -390,12 +390,20 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
     const SceneView v{sc->t,    sc->first_tab, sc->qstart,    sc->theta,    sc->coinc, sc->cpre,
                       sc->prow, sc->id,        sc->qpad,      sc->theta_pad, sc->prow_pad, sc->rfc,
                       sc->rlc,  sc->ninfo,     sc->fmax,      (int)sc->S};
-    // Windows are processed in chunks (the alpha history of a chunk must fit the
-    // budget; a smaller chunk keeps a layer L2-resident for the next step's reads).
-    // Optionally chunks alternate between two streams.
-    // alpha history per chunk: 6 GiB (HGM_HIST_GB: tuning knob)
+    // Windows are processed in chunks: the alpha history of a chunk (every layer) must fit
+    // the budget.  Larger chunks amortise each step launch's tail and each chunk's backtrack
+    // over more windows (A/B on one B200, profiles/r02b/r02ag_hist_budget_ab.txt: C3 338.4 ->
+    // 321.9 ms from 6 to 24 GiB, C2 -4.5 %, C4 T=20 -5 %; 48 GiB a further -0.7 %); a layer of
+    // a C3 chunk is far larger than L2 either way.  Budget: min(24 GiB, 1/6 of the device's
+    // memory); HGM_HIST_GB overrides (tuning).  Optionally chunks alternate between two streams.
     const char *genv = getenv("HGM_HIST_GB");
-    const int64_t budget_floats = ((genv && atoi(genv) > 0) ? (int64_t)atoi(genv) : 6) * ((int64_t)1 << 28);
+    int64_t budget_floats = (int64_t)24 << 28;
+    {
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess && tot > 0)
+            budget_floats = std::min<int64_t>(budget_floats, (int64_t)(tot / 6 / sizeof(float)));
+        if (genv && atoi(genv) > 0) budget_floats = (int64_t)atoi(genv) << 28;
+    }
     BTArgs bt{};
     bt.U = U;
     bt.Us = Us;
@@ -449,7 +457,7 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
     // chunks are few-window ones (long chains / wide windows: C4): a chunk's last DP
     // steps and its backtrack leave the GPU mostly idle, the other lane fills it
     // (C4, ~8 windows per chunk: 21-32 % less time per call).  Many-window chunks (C3,
-    // ~800 per 6 GiB chunk) are faster on one lane, and a second lane doubles the history.
+    // ~3,200 per 24 GiB chunk) are faster on one lane, and a second lane doubles the history.
     const char *senv = getenv("HGM_STREAMS");  // 1 / 2: force
     const int nlanes = lane > 0 ? 1  // a concurrent model batch: its lane is the only one
                                 : senv ? (atoi(senv) == 2 ? 2 : 1)
