@@ -412,7 +412,24 @@ hgm_status match_batch(const hgm_model *const *models, int NM, const hgm_scene *
     // a C3 chunk is far larger than L2 either way.  Budget: min(24 GiB, 1/6 of the device's
     // memory); HGM_HIST_GB overrides (tuning).  Optionally chunks alternate between two streams.
     const char *genv = getenv("HGM_HIST_GB");
+    // ... except for calls whose chunks hold few windows (the two-chunk-lane regime below,
+    // judged at 6 GiB chunks): those keep >= 12 chunks (budget >= 6 GiB) so the two lanes
+    // pipeline -- a handful of big chunks leaves the last one running alone (C4 T=20 rho=2:
+    // 226 -> 281 ms with 24 GiB chunks; C2, one lane, 304 -> 290 ms)
+    int64_t hist_total = 0;
+    {
+        const int SSb = v0 ? 1 : (win ? NM : entry_floats(NM));
+        for (const InstDesc &d : all) {
+            const int64_t ns = (int64_t)d.ntail + 2 * (int64_t)(d.we - d.wb) + 1;
+            hist_total += (win ? (ns * SSb + 3) & ~(int64_t)3 : ns * SSb) * std::max(nsteps, 1);
+        }
+    }
     int64_t budget_floats = std::min<int64_t>((int64_t)24 << 28, (int64_t)(device_total_mem(sc->device) / 6 / sizeof(float)));
+    {
+        const int64_t n6 = (hist_total + ((int64_t)6 << 28) - 1) / ((int64_t)6 << 28);  // chunks at 6 GiB
+        if (n6 >= 3 && (int64_t)count < 64 * n6)
+            budget_floats = std::min(budget_floats, std::max<int64_t>((int64_t)6 << 28, hist_total / 12));
+    }
     if (genv && atoi(genv) > 0) budget_floats = (int64_t)atoi(genv) << 28;
     BTArgs bt{};
     bt.U = U;
