@@ -707,3 +707,42 @@ def test_window_kernel_paths(hgm, capfd, monkeypatch, case):
     for j, k in enumerate(ks):
         msg = chk.check_pair(0, k, float(m0.E[k]), float(m0.A[k]), m0.z[k].cpu().numpy(), E_o[j], A_o[j], z_o[j])
         assert msg in (None, "TIE"), msg
+
+
+def test_model_builder_saliency_ties(hgm):
+    """Model chain with equal saliencies (the most salient point of each frame; reading
+    R-D1: ties keep the earliest input point).  Every model frame holds three points of equal
+    saliency (two frames also a less salient one), in shuffled input order; the scene is an
+    exact copy of the expected chain (the earliest tied point of each frame), so the GPU match
+    must give E* = A = 0 with every label real -- a builder that took another tied point sees
+    different descriptors and positions -- and it must equal the oracle's match."""
+    rng = np.random.default_rng(5)
+    F, n_frames = 16, 10
+    rows = []
+    for f in range(n_frames):
+        k = 3 + (1 if f in (2, 7) else 0)
+        for j in range(k):
+            sal = 1.0 if j < 3 else 0.5
+            rows.append((f, float(rng.integers(0, 160)), float(rng.integers(0, 120)), sal))
+    order = rng.permutation(len(rows))
+    rows = [rows[i] for i in order]
+    feat = np.abs(rng.normal(size=(len(rows), F))).astype(np.float32)
+    feat /= np.linalg.norm(feat, axis=1, keepdims=True)
+    model = synth.Points(np.array([r[0] for r in rows], np.int32), np.array([r[1] for r in rows], np.float32),
+                         np.array([r[2] for r in rows], np.float32), np.array([r[3] for r in rows], np.float32), feat)
+    first = {}
+    for i, r in enumerate(rows):  # the earliest input point of saliency 1.0 per frame
+        if r[3] == 1.0 and r[0] not in first:
+            first[r[0]] = i
+    sel = np.array([first[f] for f in range(n_frames)])
+    scene = model.take(sel)
+    scene.saliency[:] = 1.0
+    p = dict(lambda1=0.6, lambda2=0.2, lambda3=5.0, w_dummy=1.0, T=5)
+    m = hgm.build_model_graph(model, device=0)
+    sc = hgm.build_scene_index(scene, device=0, T_max=p["T"])
+    r = hgm.match_model_at_offsets(m, sc, p, 0, 1, 1, n_frames, device_out=False)
+    assert abs(float(r.E[0])) <= 1e-6 and abs(float(r.A[0])) <= 1e-6, (r.E[0], r.A[0])
+    assert (np.asarray(r.z[0]) >= 0).all(), r.z[0]
+    ref = oracle.detect([model], scene, p, 0, 1, 1, n_frames)
+    assert abs(float(r.E[0]) - float(ref.E[0, 0])) <= 1e-6 + 1e-5 * abs(float(ref.E[0, 0]))
+    assert list(r.z[0]) == list(ref.z[0, 0, :n_frames])
