@@ -210,10 +210,12 @@ static bool make_tiling(const hgm_scene *sc, const hgm_offsets &o, int T, int NM
         stages[0] = stages[1] = 1;
     if (T > 128 && !benv && !nenv) {
         // b-tiles are single frames here (FT_max = 1) and items are a-frame chunks whose
-        // fixed part (b-row entries, row tables) is amortised over the chunk: one 220 KB
-        // stage per SM (wider chunks, half the items) measured faster than two 110 KB
-        // stages or two 220 KB ones (single instance, T = 320: 7.3 -> 4.7 ms)
-        budgets[0] = std::min(budgets[2], (size_t)220 * 1024);
+        // fixed part (b-row entries, row tables) is amortised over the chunk: one single
+        // stage per CTA.  One 220 KB stage per SM measured faster than two 110 KB stages or
+        // two 220 KB ones before task splitting and programmatic dependent launch (single
+        // instance, T = 320: 7.3 -> 4.7 ms); with them, two CTAs per SM with one 110 KB
+        // stage each are faster again (T = +inf: 8.17 -> 7.47 ms, profiles/r02b/r02al_*)
+        budgets[0] = std::min(budgets[2], (size_t)110 * 1024);
         stages[0] = 1;
     }
     // stage bytes of the unclipped item: b-frames [a, b), a-frames [g0, g1)
